@@ -1,0 +1,7 @@
+"""TEST INFRASTRUCTURE ONLY: the CPU oracle for the DMV3D renderer + DDIM step.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product package
+(paper_2605_18052_b200) never imports it.
+"""
+from .oracle import *  # noqa: F401,F403

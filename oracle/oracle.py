@@ -1,0 +1,280 @@
+"""ctypes wrapper of liboracle.so (oracle/dmv3d_oracle.c).  TEST INFRASTRUCTURE ONLY.
+
+Functions mirror the paper's definitions (see dmv3d_oracle.h for citations).
+Inputs are numpy arrays; bf16 inputs must be passed as their exact float32
+upcast (paper_2605_18052_b200.workloads.bf16_bits_to_f32), so the oracle
+measures compute precision, not input quantisation.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dmv3d_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+AGG_MEAN, AGG_SUM = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so: -O2 -fopenmp -ffp-contract=off, no fast-math."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "dmv3d_oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off",
+                               "-fno-fast-math", "-fPIC", "-shared", "-D_GNU_SOURCE",
+                               "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Triplane(ct.Structure):
+    _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("data", ct.POINTER(ct.c_float)),
+                ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3)]
+
+
+class _MLP(ct.Structure):
+    _fields_ = [("num_layers", ct.c_int32), ("in_dim", ct.c_int32), ("hidden", ct.c_int32),
+                ("weights", ct.POINTER(ct.POINTER(ct.c_float))),
+                ("biases", ct.POINTER(ct.POINTER(ct.c_float))),
+                ("hidden_act", ct.c_int32), ("density_shift", ct.c_double),
+                ("rgb_widen_eps", ct.c_double)]
+
+
+class _Cameras(ct.Structure):
+    _fields_ = [("num_views", ct.c_int32), ("height", ct.c_int32), ("width", ct.c_int32),
+                ("intrinsics", ct.POINTER(ct.c_float)), ("c2w", ct.POINTER(ct.c_float))]
+
+
+class _Opts(ct.Structure):
+    _fields_ = [("samples_per_ray", ct.c_int32), ("agg", ct.c_int32), ("jitter", ct.c_int32),
+                ("seed", ct.c_uint64), ("bg", ct.c_double * 3)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ct.CDLL(build())
+        P = ct.POINTER
+        f32p, f64p = P(ct.c_float), P(ct.c_double)
+        _lib.orc_cosine_alpha_bar.argtypes = [ct.c_int32, ct.c_double, f64p]
+        _lib.orc_ray_geometry.argtypes = [P(_Cameras), f32p, f32p, ct.c_int64, f32p, f32p, f32p,
+                                          f32p, P(ct.c_int32)]
+        _lib.orc_jitter.argtypes = [ct.c_uint64, ct.c_uint64]
+        _lib.orc_jitter.restype = ct.c_float
+        _lib.orc_sample_point.argtypes = [f32p, f32p, ct.c_float, ct.c_float, ct.c_int32,
+                                          ct.c_int32, ct.c_int32, ct.c_uint64, ct.c_int64, f32p,
+                                          f32p]
+        _lib.orc_texel_coord.argtypes = [ct.c_float, ct.c_float, ct.c_float, ct.c_int32,
+                                         P(ct.c_int32), f32p]
+        _lib.orc_point_features.argtypes = [P(_Triplane), ct.c_int32, f32p, f64p]
+        _lib.orc_mlp_decode.argtypes = [P(_MLP), f64p, f64p, f64p]
+        _lib.orc_decode_point.argtypes = [P(_Triplane), P(_MLP), ct.c_int32, f32p, f64p]
+        _lib.orc_render_ray.argtypes = [P(_Triplane), P(_Cameras), P(_MLP), P(_Opts), ct.c_int64,
+                                        f64p, f64p]
+        _lib.orc_render_rays.argtypes = [P(_Triplane), P(_Cameras), P(_MLP), P(_Opts),
+                                         ct.c_int64, P(ct.c_int64), f64p, f64p, ct.c_int32]
+        _lib.orc_render_views.argtypes = [P(_Triplane), P(_Cameras), P(_MLP), P(_Opts), f64p,
+                                          f64p, ct.c_int32]
+        _lib.orc_ddim_step.argtypes = [f64p, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_double,
+                                       ct.c_double, ct.c_double, ct.c_int32, ct.c_int32,
+                                       ct.c_int32, f64p, f64p, f64p, P(ct.c_uint8), f64p]
+    return _lib
+
+
+def _fp(a):
+    return a.ctypes.data_as(ct.POINTER(ct.c_float))
+
+
+def _dp(a):
+    return a.ctypes.data_as(ct.POINTER(ct.c_double))
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class _Keep:
+    """Holds numpy buffers alive while ctypes structs point into them."""
+
+    def __init__(self):
+        self.refs = []
+
+    def __call__(self, a):
+        self.refs.append(a)
+        return a
+
+
+def _triplane(tp, keep, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    tp = keep(_f32(tp))
+    s = _Triplane(tp.shape[1], tp.shape[3], _fp(tp), (ct.c_float * 3)(*aabb_min),
+                  (ct.c_float * 3)(*aabb_max))
+    return s
+
+
+def _mlp(m, keep):
+    ws = [keep(_f32(w)) for w in m.weights]
+    bs = [keep(_f32(b)) for b in m.biases]
+    L = len(ws)
+    warr = keep((ct.POINTER(ct.c_float) * L)(*[_fp(w) for w in ws]))
+    barr = keep((ct.POINTER(ct.c_float) * L)(*[_fp(b) for b in bs]))
+    hidden = ws[0].shape[0] if L > 1 else 4
+    return _MLP(L, ws[0].shape[1], hidden, warr, barr, m.hidden_act, m.density_shift,
+                m.rgb_widen_eps)
+
+
+def _cams(c, keep):
+    intr = keep(_f32(c.intrinsics))
+    c2w = keep(_f32(c.c2w))
+    return _Cameras(c2w.shape[0], c.height, c.width, _fp(intr), _fp(c2w))
+
+
+def _opts(N, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0, 1.0, 1.0)):
+    return _Opts(N, agg, jitter, seed, (ct.c_double * 3)(*bg))
+
+
+# ------------------------------------------------------------------ API
+def cosine_alpha_bar(T: int = 1000, s: float = 0.008) -> np.ndarray:
+    out = np.zeros(T, dtype=np.float64)
+    lib().orc_cosine_alpha_bar(T, s, _dp(out))
+    return out
+
+
+def ray_geometry(cams, ray_ids, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    """fp32 geometry for ray ids -> (o [n,3], d [n,3], t_near [n], t_far [n], hit [n])."""
+    keep = _Keep()
+    c = _cams(cams, keep)
+    lo = keep(_f32(aabb_min))
+    hi = keep(_f32(aabb_max))
+    ray_ids = np.asarray(ray_ids, dtype=np.int64)
+    n = len(ray_ids)
+    o = np.zeros((n, 3), np.float32)
+    d = np.zeros((n, 3), np.float32)
+    tn = np.zeros(n, np.float32)
+    tf = np.zeros(n, np.float32)
+    hit = np.zeros(n, np.int32)
+    L = lib()
+    for q, r in enumerate(ray_ids):
+        oo, dd = np.zeros(3, np.float32), np.zeros(3, np.float32)
+        a, b = ct.c_float(), ct.c_float()
+        h = ct.c_int32()
+        L.orc_ray_geometry(ct.byref(c), _fp(lo), _fp(hi), int(r), _fp(oo), _fp(dd), ct.byref(a),
+                           ct.byref(b), ct.byref(h))
+        o[q], d[q], tn[q], tf[q], hit[q] = oo, dd, a.value, b.value, h.value
+    return o, d, tn, tf, hit
+
+
+def jitter(seed: int, sample_id: int) -> float:
+    return lib().orc_jitter(seed, sample_id)
+
+
+def sample_point(o, d, t_near, t_far, N, k, jit=0, seed=0, r=0):
+    o, d = _f32(o), _f32(d)
+    p = np.zeros(3, np.float32)
+    t = ct.c_float()
+    lib().orc_sample_point(_fp(o), _fp(d), float(t_near), float(t_far), N, k, jit, seed, r,
+                           ct.byref(t), _fp(p))
+    return np.float32(t.value), p
+
+
+def texel_coord(q, lo, hi, R):
+    i0 = ct.c_int32()
+    f = ct.c_float()
+    lib().orc_texel_coord(float(q), float(lo), float(hi), R, ct.byref(i0), ct.byref(f))
+    return i0.value, np.float32(f.value)
+
+
+def point_features(tp, points, agg=AGG_MEAN):
+    keep = _Keep()
+    t = _triplane(tp, keep)
+    pts = _f32(points).reshape(-1, 3)
+    out = np.zeros((len(pts), tp.shape[3]), np.float64)
+    for q in range(len(pts)):
+        p = np.ascontiguousarray(pts[q])
+        row = np.zeros(tp.shape[3], np.float64)
+        lib().orc_point_features(ct.byref(t), agg, _fp(p), _dp(row))
+        out[q] = row
+    return out
+
+
+def mlp_decode(m, h0):
+    keep = _Keep()
+    mm = _mlp(m, keep)
+    h0 = np.ascontiguousarray(np.atleast_2d(h0), dtype=np.float64)
+    out = np.zeros((len(h0), 4), np.float64)
+    for q in range(len(h0)):
+        s = ct.c_double()
+        rgb = np.zeros(3, np.float64)
+        lib().orc_mlp_decode(ct.byref(mm), _dp(np.ascontiguousarray(h0[q])), ct.byref(s), _dp(rgb))
+        out[q, 0] = s.value
+        out[q, 1:] = rgb
+    return out
+
+
+def decode_points(tp, m, points, agg=AGG_MEAN):
+    keep = _Keep()
+    t = _triplane(tp, keep)
+    mm = _mlp(m, keep)
+    pts = _f32(points).reshape(-1, 3)
+    out = np.zeros((len(pts), 4), np.float64)
+    for q in range(len(pts)):
+        row = np.zeros(4, np.float64)
+        lib().orc_decode_point(ct.byref(t), ct.byref(mm), agg, _fp(np.ascontiguousarray(pts[q])),
+                               _dp(row))
+        out[q] = row
+    return out
+
+
+def render_rays(tp, cams, m, N, ray_ids, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0, 1.0, 1.0),
+                threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    """Render selected ray ids -> rgb [n,3], alpha [n] (fp64)."""
+    keep = _Keep()
+    t = _triplane(tp, keep, aabb_min, aabb_max)
+    mm = _mlp(m, keep)
+    c = _cams(cams, keep)
+    o = _opts(N, agg, jitter, seed, bg)
+    ids = np.ascontiguousarray(ray_ids, dtype=np.int64)
+    rgb = np.zeros((len(ids), 3), np.float64)
+    alpha = np.zeros(len(ids), np.float64)
+    lib().orc_render_rays(ct.byref(t), ct.byref(c), ct.byref(mm), ct.byref(o), len(ids),
+                          ids.ctypes.data_as(ct.POINTER(ct.c_int64)), _dp(rgb), _dp(alpha),
+                          threads)
+    return rgb, alpha
+
+
+def render_views(tp, cams, m, N, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0, 1.0, 1.0), threads=0,
+                 aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    """Render all views -> rgb [V,3,H,W], alpha [V,H,W] (fp64)."""
+    keep = _Keep()
+    t = _triplane(tp, keep, aabb_min, aabb_max)
+    mm = _mlp(m, keep)
+    c = _cams(cams, keep)
+    o = _opts(N, agg, jitter, seed, bg)
+    V, H, W = cams.num_views, cams.height, cams.width
+    rgb = np.zeros((V, 3, H, W), np.float64)
+    alpha = np.zeros((V, H, W), np.float64)
+    lib().orc_render_views(ct.byref(t), ct.byref(c), ct.byref(mm), ct.byref(o), _dp(rgb),
+                           _dp(alpha), threads)
+    return rgb, alpha
+
+
+def ddim_step(alpha_bar, t, t_prev, x_t, x0_rgb, z=None, eta=0.0, keep_mask=None,
+              x0_scale=2.0, x0_shift=-1.0):
+    """x_{t-1} from x_t and the rendered x0 image, all [V,3,H,W] (fp64)."""
+    ab = np.ascontiguousarray(alpha_bar, dtype=np.float64)
+    x_t = np.ascontiguousarray(x_t, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0_rgb, dtype=np.float64)
+    V, _, H, W = x_t.shape
+    zz = np.ascontiguousarray(z, dtype=np.float64) if z is not None else None
+    km = np.ascontiguousarray(keep_mask, dtype=np.uint8) if keep_mask is not None else None
+    out = np.zeros_like(x_t)
+    lib().orc_ddim_step(_dp(ab), len(ab), t, t_prev, eta, x0_scale, x0_shift, V, H, W, _dp(x_t),
+                        _dp(x0), _dp(zz) if zz is not None else None,
+                        km.ctypes.data_as(ct.POINTER(ct.c_uint8)) if km is not None else None,
+                        _dp(out))
+    return out
