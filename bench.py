@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: rays/s of one DMV3D denoise step (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step is one fused pass of the whole hot path
+over one asset: render 4 input + 4 novel views at 256x256 from a
+3x64x64x80 bf16 triplane with N = 128 samples/ray through the shared
+80-64-64-64-4 MLP, composite, and apply the DDIM x_{t-1} update to the 4
+input views (cfg3).  Steps walk the paper's 50-step DDIM grid 980 -> 0
+(PAPER.md:471), feeding x_{t-1} back as the next x_t.  Multi-GPU (torchrun):
+one asset per rank (weak scaling; assets are independent), no
+data-path collective; timing is the max over ranks.
+
+Prints ONE JSON line on rank 0.  `value` = rays/s over all ranks with inputs
+resident in HBM; `e2e` = the same through the host-buffer C-ABI entry
+(pinned host in/out copies inside the timed region); `roofline` = the render
+kernel's algorithmic MLP FLOPs / its CUDA-event time vs the measured dense
+bf16 peak; `cpu_baseline` = the CPU oracle on a bounded sample of the
+same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rays/s per denoise-step render (4 input + 4 novel views 256x256, fused DDIM)"
+WORKLOAD = ("cfg3: 4 input + 4 novel views 256x256, triplane 3x64x64x80 bf16, N=128 "
+            "midpoint samples/ray, shared MLP 80-64-64-64-4 (ReLU), fused DDIM on the 4 "
+            "input views along the 50-step grid 980..0, eta=0, term_eps=1e-4, white bg")
+MLP_FLOPS_PER_SAMPLE = 2 * (80 * 64 + 2 * 64 * 64 + 64 * 4)  # 27,136
+TERM_EPS = 1e-4
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 2 + k and r[2 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_rate(w, budget_s: float, threads: int, max_rays: int = 65536, seed: int = 7):
+    """Oracle rays/s on a bounded random sample of the workload's rays."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(w.num_rays)[:max_rays]
+    done, t0, chunk = 0, time.perf_counter(), 256
+    while done < len(ids) and time.perf_counter() - t0 < budget_s:
+        oracle.render_rays(w.triplane, w.cameras, w.mlp, w.samples_per_ray, ids[done:done + chunk],
+                           threads=threads)
+        done += chunk
+        chunk = min(chunk * 2, 4096)
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on this host's cores."""
+    if rank != 0:
+        return
+    from paper_2605_18052_b200 import workloads as wl
+    w = wl.make_workload("cfg3")
+    threads = os.cpu_count() or 1
+    rays_per_step = 2048
+    import oracle
+    rng = np.random.default_rng(11)
+    times = []
+    for s in range(args.warmup + args.steps):
+        ids = rng.choice(w.num_rays, rays_per_step, replace=False)
+        t0 = time.perf_counter()
+        oracle.render_rays(w.triplane, w.cameras, w.mlp, w.samples_per_ray, ids, threads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    total = float(np.sum(times))
+    value = rays_per_step * len(times) / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "rays_per_step_sampled": rays_per_step},
+            "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{rays_per_step} random rays of cfg3 per step (of 524288), "
+                                       "full 128-sample march, fp64, no early termination"},
+            "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_18052_b200 import api, schedule
+    from paper_2605_18052_b200 import workloads as wl
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs (one asset per rank, seeds 100 + rank), resident in HBM
+    w = wl.make_workload("cfg3", asset=rank if world > 1 else None)
+    V, H, W = w.cameras.num_views, w.cameras.height, w.cameras.width
+    DV = w.ddim_views
+    tp = torch.from_numpy(w.triplane).to(dev).to(torch.bfloat16).contiguous()
+    intr = torch.from_numpy(w.cameras.intrinsics).to(dev)
+    c2w = torch.from_numpy(w.cameras.c2w).to(dev)
+    mlp = api.DeviceMLP.from_host(w.mlp, "bf16", dev)
+    ab = schedule.cosine_alpha_bar()
+    pairs = schedule.ddim_pairs(50, 1000)
+    x0 = torch.from_numpy(wl.gaussian((DV, 3, H, W), wl.SEED_XT)).to(dev)
+    xa, xb = x0.clone(), torch.empty_like(x0)
+    rgb = torch.empty((V, 3, H, W), device=dev)
+    alpha = torch.empty((V, H, W), device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev)
+    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    rays = V * H * W
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, x_in, x_out, cnt=None):
+        t, tp_ = pairs[i % len(pairs)]
+        api.dmv3d_render_ddim_step(tp, intr, c2w, H, W, mlp, ab, t, tp_, x_in, None, 0.0, None,
+                                   x_prev=x_out, rgb=rgb, alpha=alpha, samples_per_ray=w.samples_per_ray,
+                                   term_eps=TERM_EPS, engine=args.engine, counters=cnt)
+
+    # warm-up (untimed), with the kernel's own counters for evaluated samples
+    for i in range(args.warmup):
+        step(i, xa, xb, counters if i == 0 else None)
+        xa, xb = xb, xa
+    torch.cuda.synchronize()
+    cnt = counters.cpu().numpy().astype(np.float64)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps, L2 flushed between steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            step(args.warmup + k, xa, xb)
+            ends[k].record(stream)
+            xa, xb = xb, xa
+        barrier()
+    step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = rays * world * args.steps / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # ---- end-to-end through the host-buffer C-ABI entry (pinned host in/out)
+    ws = api.Workspace()
+    h_tp = tp.cpu().pin_memory()
+    h_intr, h_c2w = intr.cpu().pin_memory(), c2w.cpu().pin_memory()
+    h_mlp = api.DeviceMLP([x.cpu().pin_memory() for x in mlp.weights],
+                          [x.cpu().pin_memory() for x in mlp.biases], "bf16")
+    h_x = [x0.cpu().pin_memory(), torch.empty(x0.shape).pin_memory()]
+    h_rgb = torch.empty(rgb.shape).pin_memory()
+    h_alpha = torch.empty(alpha.shape).pin_memory()
+    h2d = (h_tp.numel() * 2 + h_intr.numel() * 4 + h_c2w.numel() * 4 + h_x[0].numel() * 4
+           + sum(x.numel() * x.element_size() for x in h_mlp.weights + h_mlp.biases))
+    d2h = h_x[0].numel() * 4 + h_rgb.numel() * 4 + h_alpha.numel() * 4
+
+    def host_step(i, a, b):
+        t, tp_ = pairs[i % len(pairs)]
+        api.dmv3d_render_ddim_step_host(ws, h_tp, h_intr, h_c2w, H, W, h_mlp, ab, t, tp_, h_x[a],
+                                        h_x[b], h_rgb, h_alpha, samples_per_ray=w.samples_per_ray,
+                                        term_eps=TERM_EPS, engine=args.engine, stream=stream)
+
+    for i in range(args.warmup):
+        host_step(i, i % 2, (i + 1) % 2)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        host_step(args.warmup + k, k % 2, (k + 1) % 2)
+        stream.synchronize()  # the step's result is read on the host
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = rays * world * args.steps / (e2e_ms / 1e3)
+    ws.close()
+
+    # ---- roofline of the dominant kernel (the fused render kernel: 1 launch / step)
+    peaks, peak_src = load_peaks()
+    hit_frac = cnt[0] / max(cnt[3], 1)
+    eval_samples = cnt[1]
+    engine_used = args.engine
+    if engine_used == "auto":
+        from paper_2605_18052_b200 import _abi
+        engine_used = "tcgen05" if _abi.lib() and _tc_available(api, tp, intr, c2w, H, W, mlp) else "simt"
+    if engine_used == "tcgen05":
+        flops = eval_samples * MLP_FLOPS_PER_SAMPLE
+        achieved = flops / (ms_per_step / 1e3) / 1e12
+        peak = peaks["bf16_tflops"]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": _ncu_traffic(engine_used),
+                "peak_source": f"{peak_src} dense bf16 (burst)",
+                "algorithmic": "27,136 MLP FLOP per evaluated sample x evaluated samples per launch"}
+        dtype = "bf16"
+    else:
+        # fp32 CUDA-core engine: MLP + gather FMAs on the FP32 pipe
+        flops = eval_samples * (MLP_FLOPS_PER_SAMPLE + 2 * 12 * 80)
+        achieved = flops / (ms_per_step / 1e3) / 1e12
+        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # 148 SMs x 128 FP32 lanes x FMA
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": _ncu_traffic(engine_used),
+                "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
+                "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per evaluated sample"}
+        dtype = "f32"
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r_rate, n_rays, secs = oracle_rate(w, args.cpu_budget, threads)
+        cpu = {"value": r_rate, "unit": "rays/s", "cores": threads, "kind": "oracle",
+               "sample": f"{n_rays} random rays of cfg3 (of {rays}) in {secs:.1f} s; full "
+                         f"128-sample march, fp64, no early termination"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+                "data": "synthetic",
+                "config": {"workload": WORKLOAD, "rays_per_step_per_gpu": rays,
+                           "assets": world, "engine": engine_used,
+                           "l2": "flushed between timed steps (256 MiB write); triplane re-read "
+                                 "from HBM each step", "parallelism": f"asset-sharded x{world}"},
+                "samples_per_s_nominal": value * w.samples_per_ray,
+                "samples_per_s_evaluated": eval_samples * world * args.steps / (total_ms / 1e3),
+                "hit_fraction": hit_frac,
+                "terminated_fraction_of_hit": cnt[2] / max(cnt[0], 1),
+                "evaluated_fraction_of_nominal": eval_samples / (rays * w.samples_per_ray),
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h)},
+                "gpu_launches": args.steps,
+                "clocks": clk.summary(), "step_ms_min": float(step_ms.min()),
+                "step_ms_median": float(np.median(step_ms))}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _tc_available(api, tp, intr, c2w, H, W, mlp):
+    try:
+        api.dmv3d_render_views(tp, intr, c2w, 1, 1, mlp, samples_per_ray=4, engine="tcgen05")
+        return True
+    except Exception:
+        return False
+
+
+def _ncu_traffic(engine):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(engine)
+    return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * dmv3d.h -- C ABI of libdmv3d.so: the B200 (sm_100a) hot path of DMV3D's
+ * reconstruction-based multi-view denoiser (arXiv 2605.18052, PAPER.md).
+ *
+ *   I_{r,t} = R(S_t, c)                                   (Eq. reconrender)
+ *   x_t = sqrt(ab_t) x_0 + sqrt(1 - ab_t) eps
+ *   x0-prediction -> x_{t-1} (DDIM)
+ *
+ * R is the triplane-NeRF renderer (Instant3D LRM
+ * PAPER.md:544): ray generation from the camera set C (a1), ray/AABB slab
+ * test on the object box [-1,1]^3 and N midpoint samples (a2),
+ * bilinear gather from the three axis-aligned planes with mean aggregation
+ * (a3), the shared MLP decoder to density and colour (a4), front-to-back
+ * compositing (a5); the DDIM step (a6) maps the rendered views to x_{t-1}.
+ * Every reading of the paper the library relies on is listed in DESIGN.md
+ * ("Readings") with its id (A1..A25).
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Tensor pointers are DEVICE pointers on the current CUDA device unless a
+ *    field says HOST.  The caller owns every buffer; the library allocates
+ *    no device memory on these calls (the *_host variant below uses a
+ *    caller-created workspace).  Inputs must stay valid until the work
+ *    enqueued on `stream` completes.
+ *  - Calls enqueue on `stream` (a cudaStream_t, 0 = legacy default stream)
+ *    and never synchronise the host.  Launch errors are returned at once as
+ *    DMV3D_ERR_CUDA; faults inside kernels surface at the caller's next sync.
+ *  - On any non-OK status nothing has been enqueued and dmv3d_last_error()
+ *    returns a thread-local message.  Re-entrant; no global mutable state.
+ *  - Layouts are C-order (row-major):
+ *      intrinsics [V][4]  fx, fy, cx, cy in pixels (pinhole, pixel centres at +1/2)
+ *      c2w        [V][3][4] camera-to-world, OpenCV axes (x right, y down, z forward)
+ *      triplane   [3][R][R][C] channels-last; planes XY, XZ, YZ; plane (a,b):
+ *                 column <- axis a, row <- axis b; align-corners texels
+ *      W_l        [out][in] (PyTorch nn.Linear), b_l [out] fp32
+ *      images     rgb [V][3][H][W], alpha [V][H][W], x_t / z / x_prev
+ *                 [ddim_views][3][H][W], fp32 (reading A25)
+ *    Ray id r = (v*H + i)*W + j; sample id = r*N + k.
+ *  - Alignment: every tensor pointer must be 16-byte aligned
+ *    (DMV3D_ERR_ALIGNMENT otherwise).
+ */
+#ifndef DMV3D_H
+#define DMV3D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *dmv3d_stream; /* == cudaStream_t */
+
+typedef enum {
+  DMV3D_OK = 0,
+  DMV3D_ERR_INVALID_ARG = 1, /* a value outside its documented range            */
+  DMV3D_ERR_UNSUPPORTED = 2, /* valid, but no kernel variant for this shape     */
+  DMV3D_ERR_CUDA = 3,        /* a CUDA runtime call / launch failed             */
+  DMV3D_ERR_ALIGNMENT = 4    /* a tensor pointer is not 16-byte aligned         */
+} dmv3d_status;
+
+typedef enum { DMV3D_F32 = 0, DMV3D_BF16 = 1 } dmv3d_dtype;
+typedef enum { DMV3D_AGG_MEAN = 0, DMV3D_AGG_SUM = 1 } dmv3d_agg;            /* A4 */
+typedef enum { DMV3D_ACT_RELU = 0, DMV3D_ACT_SILU = 1, DMV3D_ACT_SOFTPLUS = 2 } dmv3d_act;
+typedef enum {
+  DMV3D_ENGINE_AUTO = 0,   /* tensor cores when the shapes allow, else SIMT            */
+  DMV3D_ENGINE_SIMT = 1,   /* fp32 CUDA-core MLP (fp32 or bf16 storage)                */
+  DMV3D_ENGINE_TCGEN05 = 2 /* bf16 tcgen05/TMEM MLP, fp32 accumulation (bf16 only)     */
+} dmv3d_engine;
+
+/* Camera set C ("viewpoints C = {c_1..c_N}"). */
+typedef struct {
+  int32_t num_views, height, width; /* V, H, W >= 1                              */
+  const float *intrinsics;          /* [V][4]    DEVICE                           */
+  const float *c2w;                 /* [V][3][4] DEVICE                           */
+} dmv3d_cameras;
+
+/* Triplane S_t (reading A1: R = 64, C = 32 or 80). */
+typedef struct {
+  int32_t res, channels; /* R >= 2; C >= 1 (C % 4 == 0 for F32, C % 8 == 0 for BF16) */
+  dmv3d_dtype dtype;
+  const void *data;      /* [3][R][R][C] DEVICE                                   */
+  float aabb_min[3], aabb_max[3]; /* object box, default -1/+1    */
+} dmv3d_triplane;
+
+/* Shared MLP decoder (reading A5-A7).  Layer l maps
+ * in_l -> out_l with in_0 = in_dim (= channels), out_{L-1} = 4 (sigma, r, g, b),
+ * every other width = hidden.  sigma = softplus(o_0 + density_shift);
+ * c = sigmoid(o_{1..3}) * (1 + 2 eps) - eps. */
+typedef struct {
+  int32_t num_layers, in_dim, hidden; /* 2 <= L <= 8                                */
+  dmv3d_dtype dtype;                  /* weight storage; biases are always fp32     */
+  const void *const *weights;         /* HOST array of L DEVICE pointers, W_l [out][in] */
+  const float *const *biases;         /* HOST array of L DEVICE pointers, b_l [out]     */
+  dmv3d_act hidden_act;
+  float density_shift, rgb_widen_eps;
+} dmv3d_mlp;
+
+/* Ray-marching options (readings A9-A14). */
+typedef struct {
+  int32_t samples_per_ray; /* N, 1 <= N <= 1024 (BASELINE: 128)                       */
+  dmv3d_agg agg;
+  int32_t jitter;          /* 0: midpoints; 1: stratified, splitmix64(seed, r*N+k)      */
+  uint64_t seed;
+  float bg_rgb[3];         /* background, default white                 */
+  float term_eps;          /* early ray termination when T < term_eps; 0 disables.
+                              |rgb - rgb_full|, |A - A_full| <= term_eps (A14)         */
+  int64_t ray_begin, ray_end; /* shard [begin, end) of global ray ids; -1,-1 = all.
+                              Only pixels of the shard are written.                    */
+  dmv3d_engine engine;
+  unsigned long long *counters; /* optional DEVICE [4] accumulators (NULL = off):
+                              [0] rays hit, [1] samples evaluated,
+                              [2] rays terminated early, [3] rays processed           */
+} dmv3d_render_opts;
+
+/* DDIM x0 -> x_{t-1} (readings A15-A20). */
+typedef struct {
+  const double *alpha_bar; /* HOST [T], 0-based alpha_bar_t in (0,1], decreasing    */
+  int32_t T, t, t_prev;    /* 0 <= t < T, -1 <= t_prev < t (t_prev = -1: ab_p = 1)   */
+  float eta;               /* [0,1]; eta > 0 needs z                                */
+  float x0_scale, x0_shift;/* x0_hat = scale * rgb + shift (default 2, -1)           */
+  const uint8_t *keep_mask;/* HOST [ddim_views] or NULL: 1 = view kept noise-free,
+                              x_{t-1} = x_t (image conditioning)        */
+  int32_t ddim_views;      /* views [0, ddim_views) of the camera set get the update;
+                              1 <= ddim_views <= min(V, 64)                          */
+} dmv3d_ddim_params;
+
+/* ---------------------------------------------------------------- renderer */
+/* R(S, c) for every view of `cams`: rgb [V][3][H][W] (required), alpha
+ * [V][H][W] (NULL = not written). */
+dmv3d_status dmv3d_render_views(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
+                                float *rgb, float *alpha, dmv3d_stream stream);
+
+/* Standalone DDIM step over [V][3][H][W]: x_prev from x_t and the rendered x0
+ * image x0_rgb.  z may be NULL iff eta == 0.  params->ddim_views is ignored
+ * (V is given); keep_mask, when set, has V entries. */
+dmv3d_status dmv3d_ddim_step(const dmv3d_ddim_params *params, int32_t V, int32_t H, int32_t W,
+                             const float *x_t, const float *x0_rgb, const float *z,
+                             float *x_prev, dmv3d_stream stream);
+
+/* One denoising step, fused: render all views of `cams` and, for the first
+ * ddim_views views, apply the DDIM update in the per-ray epilogue.
+ * x_t, z (NULL iff eta == 0), x_prev: [ddim_views][3][H][W].
+ * rgb [V][3][H][W] and alpha [V][H][W] may each be NULL; when rgb is NULL the
+ * views >= ddim_views are rendered for nothing, so pass V == ddim_views. */
+dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                    const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
+                                    const dmv3d_ddim_params *ddim, const float *x_t,
+                                    const float *z, float *x_prev, float *rgb, float *alpha,
+                                    dmv3d_stream stream);
+
+/* ------------------------------------------------------ host-buffer variant */
+/* Same step with every tensor pointer (triplane data, weights, biases,
+ * intrinsics, c2w, x_t, z, x_prev, rgb, alpha) a HOST pointer (pinned for
+ * async copies).  The workspace owns grow-only device buffers; one
+ * workspace per thread/stream.  Copies in, launches, copies out, all on
+ * `stream`; the host buffers are valid after the stream is synchronised. */
+typedef struct dmv3d_workspace dmv3d_workspace;
+dmv3d_status dmv3d_workspace_create(dmv3d_workspace **ws);
+dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws);
+dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_triplane *triplane,
+                                         const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                         const dmv3d_render_opts *opts,
+                                         const dmv3d_ddim_params *ddim, const float *x_t,
+                                         const float *z, float *x_prev, float *rgb,
+                                         float *alpha, dmv3d_stream stream);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char *dmv3d_last_error(void);
+/* Library version string. */
+const char *dmv3d_version(void);
+
+/* ----------------------------------------------- stage-level entry points */
+/* Bit-exact geometry for rays [ray_begin, ray_end) of opts (all when -1):
+ * o_d [n][6] (origin, unit direction), tn_tf [n][2], hit [n] (0/1).  Misses
+ * report t_near = t_far = 0.  Any output may be NULL. */
+dmv3d_status dmv3d_debug_ray_geometry(const dmv3d_cameras *cams, const float aabb_min[3],
+                                      const float aabb_max[3], const dmv3d_render_opts *opts,
+                                      float *o_d, float *tn_tf, uint8_t *hit,
+                                      dmv3d_stream stream);
+/* Bit-exact sample set: t_k [n][N], point [n][N][3], texel [n][N][3][2]
+ * (column, row index per plane), frac [n][N][3][2] (fractions); rays that
+ * miss write zeros; `res` is the triplane resolution R.  Any output may be NULL. */
+dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const float aabb_min[3],
+                                       const float aabb_max[3], int32_t res,
+                                       const dmv3d_render_opts *opts,
+                                       float *t_k, float *points, int32_t *texel, float *frac,
+                                       dmv3d_stream stream);
+/* Aggregated triplane features at n points [n][3] -> feats [n][C] (fp32 math). */
+dmv3d_status dmv3d_debug_sample_features(const dmv3d_triplane *triplane, dmv3d_agg agg,
+                                         int64_t n, const float *points, float *feats,
+                                         dmv3d_stream stream);
+/* Gather + MLP decode at n points -> sigma_rgb [n][4] (engine SIMT, fp32 math). */
+dmv3d_status dmv3d_debug_decode(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                dmv3d_agg agg, int64_t n, const float *points,
+                                float *sigma_rgb, dmv3d_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMV3D_H */

@@ -1,0 +1,253 @@
+"""Python binding of libdmv3d (same names as the C ABI, argument marshalling only).
+
+PyTorch supplies device memory and the current CUDA stream; every step of the
+path (rays, samples, gather, MLP, compositing, DDIM) runs in libdmv3d's
+kernels.  There is no fallback: a missing library or a non-OK status raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _abi
+
+_DT = {"f32": _abi.F32, "bf16": _abi.BF16}
+_TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+_ENGINE = {"auto": _abi.ENGINE_AUTO, "simt": _abi.ENGINE_SIMT, "tcgen05": _abi.ENGINE_TCGEN05}
+_AGG = {"mean": _abi.AGG_MEAN, "sum": _abi.AGG_SUM}
+
+
+def _ptr(t):
+    return None if t is None else ct.c_void_p(t.data_ptr())
+
+
+def _stream(device=None):
+    return ct.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+@dataclasses.dataclass
+class DeviceMLP:
+    """Shared MLP on the device: weights W_l [out][in] (f32 or bf16), biases f32."""
+    weights: list
+    biases: list
+    dtype: str
+    hidden_act: int = 0
+    density_shift: float = 0.0
+    rgb_widen_eps: float = 0.0
+
+    @classmethod
+    def from_host(cls, m, dtype: str = "f32", device="cuda"):
+        ws = [torch.from_numpy(np.ascontiguousarray(w)).to(device=device, dtype=_TORCH_DT[dtype])
+              for w in m.weights]
+        bs = [torch.from_numpy(np.ascontiguousarray(b, dtype=np.float32)).to(device) for b in m.biases]
+        return cls(ws, bs, dtype, m.hidden_act, m.density_shift, m.rgb_widen_eps)
+
+    def struct(self, keep):
+        L = len(self.weights)
+        warr = (ct.c_void_p * L)(*[w.data_ptr() for w in self.weights])
+        barr = (ct.c_void_p * L)(*[b.data_ptr() for b in self.biases])
+        keep += [warr, barr]
+        hidden = int(self.weights[0].shape[0]) if L > 1 else 4
+        return _abi.MLP(L, int(self.weights[0].shape[1]), hidden, _DT[self.dtype],
+                        ct.cast(warr, ct.POINTER(ct.c_void_p)), ct.cast(barr, ct.POINTER(ct.c_void_p)),
+                        self.hidden_act, self.density_shift, self.rgb_widen_eps)
+
+
+def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0, 1.0, 1.0)):
+    assert tp.dim() == 4 and tp.shape[0] == 3 and tp.shape[1] == tp.shape[2] and tp.is_contiguous()
+    dt = {torch.float32: _abi.F32, torch.bfloat16: _abi.BF16}[tp.dtype]
+    return _abi.Triplane(int(tp.shape[1]), int(tp.shape[3]), dt, tp.data_ptr(),
+                         (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max))
+
+
+def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, width: int):
+    assert intrinsics.dtype == torch.float32 and c2w.dtype == torch.float32
+    assert intrinsics.is_contiguous() and c2w.is_contiguous()
+    return _abi.Cameras(int(c2w.shape[0]), height, width, intrinsics.data_ptr(), c2w.data_ptr())
+
+
+def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
+                term_eps=0.0, ray_range=None, engine="auto", counters=None):
+    b, e = (-1, -1) if ray_range is None else ray_range
+    return _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
+                           (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
+                           None if counters is None else counters.data_ptr())
+
+
+def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mask, ddim_views,
+                keep, x0_scale=2.0, x0_shift=-1.0):
+    ab = np.ascontiguousarray(alpha_bar, dtype=np.float64)
+    keep.append(ab)
+    km = None
+    if keep_mask is not None:
+        km = np.ascontiguousarray(keep_mask, dtype=np.uint8)
+        keep.append(km)
+    return _abi.DdimParams(ab.ctypes.data_as(ct.POINTER(ct.c_double)), len(ab), t, t_prev, eta,
+                           x0_scale, x0_shift,
+                           km.ctypes.data_as(ct.POINTER(ct.c_uint8)) if km is not None else None,
+                           ddim_views)
+
+
+# ------------------------------------------------------------------- entry points
+def dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP, rgb=None,
+                       alpha=None, aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, **opts):
+    """R(S, c) for every view -> rgb [V,3,H,W], alpha [V,H,W]."""
+    V = int(c2w.shape[0])
+    dev = triplane.device
+    if rgb is None:
+        rgb = torch.empty((V, 3, height, width), device=dev, dtype=torch.float32)
+    if alpha is None:
+        alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
+    keep = []
+    t = triplane_struct(triplane, aabb_min, aabb_max)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    o = opts_struct(**opts)
+    _abi.check(_abi.lib().dmv3d_render_views(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o),
+                                             _ptr(rgb), _ptr(alpha), _stream(dev)))
+    return rgb, alpha
+
+
+def dmv3d_ddim_step(alpha_bar, t, t_prev, x_t, x0_rgb, z=None, eta=0.0, keep_mask=None,
+                    x_prev=None, x0_scale=2.0, x0_shift=-1.0):
+    """Standalone DDIM x0 -> x_{t-1} over [V,3,H,W]."""
+    V, _, H, W = x_t.shape
+    if x_prev is None:
+        x_prev = torch.empty_like(x_t)
+    keep = []
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, V, keep, x0_scale, x0_shift)
+    _abi.check(_abi.lib().dmv3d_ddim_step(ct.byref(d), V, H, W, _ptr(x_t), _ptr(x0_rgb), _ptr(z),
+                                          _ptr(x_prev), _stream(x_t.device)))
+    return x_prev
+
+
+def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP, alpha_bar,
+                           t, t_prev, x_t, z=None, eta=0.0, keep_mask=None, x_prev=None,
+                           rgb=None, alpha=None, want_rgb=True, want_alpha=True,
+                           aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, x0_scale=2.0,
+                           x0_shift=-1.0, **opts):
+    """Fused step: render all views; views [0, x_t.shape[0]) also get x_{t-1}."""
+    V = int(c2w.shape[0])
+    dv = int(x_t.shape[0])
+    dev = triplane.device
+    if x_prev is None:
+        x_prev = torch.empty_like(x_t)
+    if rgb is None and want_rgb:
+        rgb = torch.empty((V, 3, height, width), device=dev, dtype=torch.float32)
+    if alpha is None and want_alpha:
+        alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
+    keep = []
+    tt = triplane_struct(triplane, aabb_min, aabb_max)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    o = opts_struct(**opts)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift)
+    _abi.check(_abi.lib().dmv3d_render_ddim_step(ct.byref(tt), ct.byref(c), ct.byref(m),
+                                                 ct.byref(o), ct.byref(d), _ptr(x_t), _ptr(z),
+                                                 _ptr(x_prev), _ptr(rgb), _ptr(alpha),
+                                                 _stream(dev)))
+    return x_prev, rgb, alpha
+
+
+class Workspace:
+    """Owner of the library's grow-only device buffers for the host-buffer entry."""
+
+    def __init__(self):
+        self.handle = ct.c_void_p()
+        _abi.check(_abi.lib().dmv3d_workspace_create(ct.byref(self.handle)))
+
+    def close(self):
+        if self.handle:
+            _abi.lib().dmv3d_workspace_destroy(self.handle)
+            self.handle = ct.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dmv3d_render_ddim_step_host(ws: Workspace, triplane, intrinsics, c2w, height, width, mlp,
+                                alpha_bar, t, t_prev, x_t, x_prev, rgb=None, alpha=None, z=None,
+                                eta=0.0, keep_mask=None, stream=None, **opts):
+    """Host-buffer step: every tensor is a (pinned) CPU tensor; copies in/out are inside
+    the library call, on `stream` (default: torch's current stream)."""
+    keep = []
+    tt = triplane_struct(triplane)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    o = opts_struct(**opts)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, int(x_t.shape[0]), keep)
+    st = ct.c_void_p(stream.cuda_stream) if stream is not None else _stream()
+    _abi.check(_abi.lib().dmv3d_render_ddim_step_host(ws.handle, ct.byref(tt), ct.byref(c),
+                                                      ct.byref(m), ct.byref(o), ct.byref(d),
+                                                      _ptr(x_t), _ptr(z), _ptr(x_prev),
+                                                      _ptr(rgb), _ptr(alpha), st))
+    return x_prev, rgb, alpha
+
+
+# ------------------------------------------------------------ stage-level (debug)
+def dmv3d_debug_ray_geometry(intrinsics, c2w, height, width, aabb_min=(-1.0,) * 3,
+                             aabb_max=(1.0,) * 3, ray_range=None):
+    V = int(c2w.shape[0])
+    n = V * height * width if ray_range is None else ray_range[1] - ray_range[0]
+    dev = c2w.device
+    o_d = torch.empty((n, 6), device=dev)
+    tn_tf = torch.empty((n, 2), device=dev)
+    hit = torch.empty((n,), device=dev, dtype=torch.uint8)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    o = opts_struct(ray_range=ray_range)
+    lo, hi = (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max)
+    _abi.check(_abi.lib().dmv3d_debug_ray_geometry(ct.byref(c), lo, hi, ct.byref(o), _ptr(o_d),
+                                                   _ptr(tn_tf), _ptr(hit), _stream(dev)))
+    return o_d, tn_tf, hit
+
+
+def dmv3d_debug_sample_points(intrinsics, c2w, height, width, res, samples_per_ray,
+                              aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, ray_range=None,
+                              jitter=False, seed=0):
+    V = int(c2w.shape[0])
+    n = V * height * width if ray_range is None else ray_range[1] - ray_range[0]
+    N = samples_per_ray
+    dev = c2w.device
+    t_k = torch.empty((n, N), device=dev)
+    pts = torch.empty((n, N, 3), device=dev)
+    texel = torch.empty((n, N, 3, 2), device=dev, dtype=torch.int32)
+    frac = torch.empty((n, N, 3, 2), device=dev)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    o = opts_struct(samples_per_ray=N, ray_range=ray_range, jitter=jitter, seed=seed)
+    lo, hi = (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max)
+    _abi.check(_abi.lib().dmv3d_debug_sample_points(ct.byref(c), lo, hi, res, ct.byref(o),
+                                                    _ptr(t_k), _ptr(pts), _ptr(texel),
+                                                    _ptr(frac), _stream(dev)))
+    return t_k, pts, texel, frac
+
+
+def dmv3d_debug_sample_features(triplane, points, agg="mean"):
+    n = int(points.shape[0])
+    feats = torch.empty((n, int(triplane.shape[3])), device=triplane.device)
+    t = triplane_struct(triplane)
+    _abi.check(_abi.lib().dmv3d_debug_sample_features(ct.byref(t), _AGG[agg], n, _ptr(points),
+                                                      _ptr(feats), _stream(triplane.device)))
+    return feats
+
+
+def dmv3d_debug_decode(triplane, mlp: DeviceMLP, points, agg="mean"):
+    n = int(points.shape[0])
+    out = torch.empty((n, 4), device=triplane.device)
+    keep = []
+    t = triplane_struct(triplane)
+    m = mlp.struct(keep)
+    _abi.check(_abi.lib().dmv3d_debug_decode(ct.byref(t), ct.byref(m), _AGG[agg], n, _ptr(points),
+                                             _ptr(out), _stream(triplane.device)))
+    return out
+
+
+# short aliases (the C names above are the canonical ones)
+render_views = dmv3d_render_views
+ddim_step = dmv3d_ddim_step
+render_ddim_step = dmv3d_render_ddim_step

@@ -1,0 +1,515 @@
+// api.cu -- the C ABI of libdmv3d.so (include/dmv3d.h): argument validation,
+// launch-parameter marshalling, engine dispatch, the host-buffer workspace.
+// No torch types; no device allocation on the device-pointer entry points.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dmv3d.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace dmv3d;
+
+namespace {
+
+thread_local std::string g_err;
+
+dmv3d_status fail(dmv3d_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+#define CHECK_ARG(cond, msg) \
+  do {                       \
+    if (!(cond)) return fail(DMV3D_ERR_INVALID_ARG, msg); \
+  } while (0)
+#define CHECK_ALIGN(p, name) \
+  do {                       \
+    if (!aligned16(p)) return fail(DMV3D_ERR_ALIGNMENT, std::string(name) + " is not 16-byte aligned"); \
+  } while (0)
+
+dmv3d_status check_cams(const dmv3d_cameras *c) {
+  CHECK_ARG(c != nullptr, "cameras is NULL");
+  CHECK_ARG(c->num_views >= 1 && c->height >= 1 && c->width >= 1, "cameras: V, H, W must be >= 1");
+  CHECK_ARG((int64_t)c->num_views * c->height * c->width < (int64_t(1) << 40), "cameras: too many rays");
+  CHECK_ARG(c->intrinsics && c->c2w, "cameras: intrinsics / c2w is NULL");
+  CHECK_ALIGN(c->intrinsics, "cameras.intrinsics");
+  CHECK_ALIGN(c->c2w, "cameras.c2w");
+  return DMV3D_OK;
+}
+
+dmv3d_status check_aabb(const float lo[3], const float hi[3]) {
+  for (int a = 0; a < 3; ++a)
+    CHECK_ARG(isfinite(lo[a]) && isfinite(hi[a]) && hi[a] > lo[a], "aabb: need finite lo < hi");
+  return DMV3D_OK;
+}
+
+dmv3d_status check_triplane(const dmv3d_triplane *t) {
+  CHECK_ARG(t != nullptr, "triplane is NULL");
+  CHECK_ARG(t->res >= 2 && t->res <= 8192, "triplane: res must be in [2, 8192]");
+  CHECK_ARG(t->channels >= 1, "triplane: channels must be >= 1");
+  CHECK_ARG(t->dtype == DMV3D_F32 || t->dtype == DMV3D_BF16, "triplane: bad dtype");
+  CHECK_ARG(t->data != nullptr, "triplane: data is NULL");
+  CHECK_ALIGN(t->data, "triplane.data");
+  if (t->dtype == DMV3D_F32 && t->channels % 4)
+    return fail(DMV3D_ERR_UNSUPPORTED, "triplane: fp32 needs channels % 4 == 0 (16-byte vectors)");
+  if (t->dtype == DMV3D_BF16 && t->channels % 8)
+    return fail(DMV3D_ERR_UNSUPPORTED, "triplane: bf16 needs channels % 8 == 0 (16-byte vectors)");
+  return check_aabb(t->aabb_min, t->aabb_max);
+}
+
+dmv3d_status check_mlp(const dmv3d_mlp *m, const dmv3d_triplane *t) {
+  CHECK_ARG(m != nullptr, "mlp is NULL");
+  CHECK_ARG(m->num_layers >= 2 && m->num_layers <= kMaxLayers, "mlp: num_layers must be in [2, 8]");
+  CHECK_ARG(m->in_dim == t->channels, "mlp: in_dim must equal triplane channels (mean/sum aggregation)");
+  CHECK_ARG(m->hidden >= 1, "mlp: hidden must be >= 1");
+  CHECK_ARG(m->dtype == DMV3D_F32 || m->dtype == DMV3D_BF16, "mlp: bad dtype");
+  CHECK_ARG(m->hidden_act >= DMV3D_ACT_RELU && m->hidden_act <= DMV3D_ACT_SOFTPLUS, "mlp: bad hidden_act");
+  CHECK_ARG(m->weights && m->biases, "mlp: weights / biases array is NULL");
+  CHECK_ARG(isfinite(m->density_shift) && isfinite(m->rgb_widen_eps), "mlp: non-finite shift/eps");
+  for (int l = 0; l < m->num_layers; ++l) {
+    CHECK_ARG(m->weights[l] && m->biases[l], "mlp: a layer pointer is NULL");
+    CHECK_ALIGN(m->weights[l], "mlp.weights[l]");
+    CHECK_ALIGN(m->biases[l], "mlp.biases[l]");
+  }
+  return DMV3D_OK;
+}
+
+dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
+  CHECK_ARG(o != nullptr, "opts is NULL");
+  CHECK_ARG(o->samples_per_ray >= 1 && o->samples_per_ray <= 1024, "opts: samples_per_ray must be in [1, 1024]");
+  CHECK_ARG(o->agg == DMV3D_AGG_MEAN || o->agg == DMV3D_AGG_SUM, "opts: bad agg");
+  CHECK_ARG(o->term_eps >= 0.0f && o->term_eps < 1.0f, "opts: term_eps must be in [0, 1)");
+  CHECK_ARG(o->engine >= DMV3D_ENGINE_AUTO && o->engine <= DMV3D_ENGINE_TCGEN05, "opts: bad engine");
+  for (int c = 0; c < 3; ++c) CHECK_ARG(isfinite(o->bg_rgb[c]), "opts: non-finite bg");
+  const bool all = o->ray_begin == -1 && o->ray_end == -1;
+  CHECK_ARG(all || (o->ray_begin >= 0 && o->ray_begin <= o->ray_end && o->ray_end <= nrays),
+            "opts: ray range must be -1,-1 or 0 <= begin <= end <= V*H*W");
+  if (o->counters) CHECK_ALIGN(o->counters, "opts.counters");
+  return DMV3D_OK;
+}
+
+void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *c,
+                 const dmv3d_mlp *m, const dmv3d_render_opts *o) {
+  memset(&P, 0, sizeof(P));
+  P.V = c->num_views;
+  P.H = c->height;
+  P.W = c->width;
+  P.intr = c->intrinsics;
+  P.c2w = c->c2w;
+  P.R = t->res;
+  P.C = t->channels;
+  P.tp = t->data;
+  for (int a = 0; a < 3; ++a) {
+    P.lo[a] = t->aabb_min[a];
+    P.hi[a] = t->aabb_max[a];
+  }
+  if (m) {
+    P.L = m->num_layers;
+    P.K = m->in_dim;
+    P.HD = m->hidden;
+    for (int l = 0; l < m->num_layers; ++l) {
+      P.w[l] = m->weights[l];
+      P.b[l] = m->biases[l];
+    }
+    P.act = m->hidden_act;
+    P.dshift = m->density_shift;
+    P.weps = m->rgb_widen_eps;
+  }
+  if (o) {
+    P.N = o->samples_per_ray;
+    P.agg = o->agg;
+    P.jitter = o->jitter ? 1 : 0;
+    P.seed = o->seed;
+    for (int ch = 0; ch < 3; ++ch) P.bg[ch] = o->bg_rgb[ch];
+    P.term_eps = o->term_eps;
+    const int64_t nrays = (int64_t)P.V * P.H * P.W;
+    P.ray_begin = (o->ray_begin == -1 && o->ray_end == -1) ? 0 : o->ray_begin;
+    P.ray_end = (o->ray_begin == -1 && o->ray_end == -1) ? nrays : o->ray_end;
+    P.counters = o->counters;
+  }
+}
+
+dmv3d_status ddim_coefficients(const dmv3d_ddim_params *d, int32_t nviews, DdimCoef &c) {
+  CHECK_ARG(d != nullptr, "ddim params is NULL");
+  CHECK_ARG(d->alpha_bar != nullptr, "ddim: alpha_bar is NULL");
+  CHECK_ARG(d->T >= 1 && d->t >= 0 && d->t < d->T, "ddim: need 0 <= t < T");
+  CHECK_ARG(d->t_prev >= -1 && d->t_prev < d->t, "ddim: need -1 <= t_prev < t");
+  CHECK_ARG(d->eta >= 0.0f && d->eta <= 1.0f, "ddim: eta must be in [0, 1]");
+  CHECK_ARG(isfinite(d->x0_scale) && isfinite(d->x0_shift), "ddim: non-finite x0 scale/shift");
+  const double ab_t = d->alpha_bar[d->t];
+  const double ab_p = d->t_prev >= 0 ? d->alpha_bar[d->t_prev] : 1.0;
+  CHECK_ARG(ab_t > 0.0 && ab_t < 1.0, "ddim: alpha_bar[t] must be in (0, 1)");
+  CHECK_ARG(ab_p > 0.0 && ab_p <= 1.0 && ab_p >= ab_t, "ddim: need alpha_bar[t] <= alpha_bar[t_prev] <= 1");
+  const double sigma = (double)d->eta * sqrt((1.0 - ab_p) / (1.0 - ab_t)) * sqrt(1.0 - ab_t / ab_p);
+  double c2 = 1.0 - ab_p - sigma * sigma;
+  if (c2 < 0.0) c2 = 0.0;
+  c.x0_scale = d->x0_scale;
+  c.x0_shift = d->x0_shift;
+  c.sqrt_ab_t = (float)sqrt(ab_t);
+  c.inv_sqrt_1m_ab_t = (float)(1.0 / sqrt(1.0 - ab_t));
+  c.sqrt_ab_p = (float)sqrt(ab_p);
+  c.c_eps = (float)sqrt(c2);
+  c.sigma_t = (float)sigma;
+  c.keep_bits = 0;
+  if (d->keep_mask) {
+    if (nviews > 64) return fail(DMV3D_ERR_UNSUPPORTED, "ddim: keep_mask supports at most 64 views");
+    for (int v = 0; v < nviews; ++v)
+      if (d->keep_mask[v]) c.keep_bits |= (1ull << v);
+  }
+  return DMV3D_OK;
+}
+
+enum class Engine { SIMT, TC };
+
+dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3d_render_opts *o,
+                         Engine &e) {
+  const bool bf16 = t->dtype == DMV3D_BF16 && m->dtype == DMV3D_BF16;
+  const bool tc_ok = bf16 && tc_supported(m->in_dim, m->hidden, m->num_layers);
+  if (o->engine == DMV3D_ENGINE_TCGEN05) {
+    if (!tc_ok)
+      return fail(DMV3D_ERR_UNSUPPORTED,
+                  "engine TCGEN05 needs bf16 triplane + weights and a supported (in_dim, hidden, L)");
+    e = Engine::TC;
+    return DMV3D_OK;
+  }
+  if (o->engine == DMV3D_ENGINE_AUTO && tc_ok && m->hidden_act == DMV3D_ACT_RELU) {
+    e = Engine::TC;
+    return DMV3D_OK;
+  }
+  if (!simt_supported(m->in_dim, m->hidden))
+    return fail(DMV3D_ERR_UNSUPPORTED, "SIMT engine: unsupported (in_dim, hidden) = (" +
+                                           std::to_string(m->in_dim) + ", " + std::to_string(m->hidden) + ")");
+  e = Engine::SIMT;
+  return DMV3D_OK;
+}
+
+dmv3d_status cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return DMV3D_OK;
+  return fail(DMV3D_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const dmv3d_mlp *m,
+                         const dmv3d_render_opts *o, const dmv3d_ddim_params *d, const float *x_t,
+                         const float *z, float *x_prev, float *rgb, float *alpha,
+                         cudaStream_t st) {
+  dmv3d_status s;
+  if ((s = check_cams(c)) != DMV3D_OK) return s;
+  if ((s = check_triplane(t)) != DMV3D_OK) return s;
+  if ((s = check_mlp(m, t)) != DMV3D_OK) return s;
+  const int64_t nrays = (int64_t)c->num_views * c->height * c->width;
+  if ((s = check_opts(o, nrays)) != DMV3D_OK) return s;
+  if (rgb) CHECK_ALIGN(rgb, "rgb");
+  if (alpha) CHECK_ALIGN(alpha, "alpha");
+  RenderParams P;
+  fill_common(P, t, c, m, o);
+  P.rgb = rgb;
+  P.alpha = alpha;
+  if (d) {
+    CHECK_ARG(d->ddim_views >= 1 && d->ddim_views <= c->num_views, "ddim: need 1 <= ddim_views <= V");
+    if (d->ddim_views > 64) return fail(DMV3D_ERR_UNSUPPORTED, "ddim: at most 64 DDIM views per call");
+    DdimCoef k;
+    if ((s = ddim_coefficients(d, d->ddim_views, k)) != DMV3D_OK) return s;
+    CHECK_ARG(x_t && x_prev, "ddim: x_t / x_prev is NULL");
+    CHECK_ARG(k.sigma_t == 0.0f || z != nullptr, "ddim: eta > 0 needs z");
+    CHECK_ALIGN(x_t, "x_t");
+    CHECK_ALIGN(x_prev, "x_prev");
+    if (z) CHECK_ALIGN(z, "z");
+    P.ddim_views = d->ddim_views;
+    P.keep_bits = k.keep_bits;
+    P.x_t = x_t;
+    P.z = z;
+    P.x_prev = x_prev;
+    P.x0_scale = k.x0_scale;
+    P.x0_shift = k.x0_shift;
+    P.sqrt_ab_t = k.sqrt_ab_t;
+    P.inv_sqrt_1m_ab_t = k.inv_sqrt_1m_ab_t;
+    P.sqrt_ab_p = k.sqrt_ab_p;
+    P.c_eps = k.c_eps;
+    P.sigma_t = k.sigma_t;
+  } else {
+    CHECK_ARG(rgb != nullptr, "rgb is NULL");
+  }
+  Engine e;
+  if ((s = pick_engine(t, m, o, e)) != DMV3D_OK) return s;
+  cudaError_t ce;
+  if (e == Engine::TC)
+    ce = launch_render_tc(P, st);
+  else
+    ce = launch_render_simt(P, t->dtype == DMV3D_BF16, m->dtype == DMV3D_BF16, st);
+  return cuda_status(ce, "render launch");
+}
+
+}  // namespace
+
+// =========================================================== exported ABI
+extern "C" {
+
+const char *dmv3d_last_error(void) { return g_err.c_str(); }
+const char *dmv3d_version(void) { return "dmv3d-b200 0.1 (sm_100a)"; }
+
+dmv3d_status dmv3d_render_views(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                const dmv3d_mlp *mlp, const dmv3d_render_opts *opts, float *rgb,
+                                float *alpha, dmv3d_stream stream) {
+  g_err.clear();
+  return render_impl(triplane, cams, mlp, opts, nullptr, nullptr, nullptr, nullptr, rgb, alpha,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                    const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
+                                    const dmv3d_ddim_params *ddim, const float *x_t,
+                                    const float *z, float *x_prev, float *rgb, float *alpha,
+                                    dmv3d_stream stream) {
+  g_err.clear();
+  if (!ddim) return fail(DMV3D_ERR_INVALID_ARG, "ddim params is NULL");
+  return render_impl(triplane, cams, mlp, opts, ddim, x_t, z, x_prev, rgb, alpha,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+dmv3d_status dmv3d_ddim_step(const dmv3d_ddim_params *params, int32_t V, int32_t H, int32_t W,
+                             const float *x_t, const float *x0_rgb, const float *z, float *x_prev,
+                             dmv3d_stream stream) {
+  g_err.clear();
+  CHECK_ARG(V >= 1 && H >= 1 && W >= 1, "ddim_step: V, H, W must be >= 1");
+  DdimCoef k;
+  dmv3d_status s = ddim_coefficients(params, V, k);
+  if (s != DMV3D_OK) return s;
+  CHECK_ARG(x_t && x0_rgb && x_prev, "ddim_step: x_t / x0_rgb / x_prev is NULL");
+  CHECK_ARG(k.sigma_t == 0.0f || z != nullptr, "ddim_step: eta > 0 needs z");
+  CHECK_ALIGN(x_t, "x_t");
+  CHECK_ALIGN(x0_rgb, "x0_rgb");
+  CHECK_ALIGN(x_prev, "x_prev");
+  if (z) CHECK_ALIGN(z, "z");
+  return cuda_status(launch_ddim(k, V, H, W, x_t, x0_rgb, z, nullptr, x_prev,
+                                 reinterpret_cast<cudaStream_t>(stream)),
+                     "ddim launch");
+}
+
+dmv3d_status dmv3d_debug_ray_geometry(const dmv3d_cameras *cams, const float aabb_min[3],
+                                      const float aabb_max[3], const dmv3d_render_opts *opts,
+                                      float *o_d, float *tn_tf, uint8_t *hit,
+                                      dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_cams(cams)) != DMV3D_OK) return s;
+  CHECK_ARG(aabb_min && aabb_max, "aabb is NULL");
+  if ((s = check_aabb(aabb_min, aabb_max)) != DMV3D_OK) return s;
+  if ((s = check_opts(opts, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
+    return s;
+  dmv3d_triplane t{};
+  t.res = 2;
+  t.channels = 4;
+  for (int a = 0; a < 3; ++a) {
+    t.aabb_min[a] = aabb_min[a];
+    t.aabb_max[a] = aabb_max[a];
+  }
+  RenderParams P;
+  fill_common(P, &t, cams, nullptr, opts);
+  return cuda_status(launch_ray_geometry(P, o_d, tn_tf, hit, reinterpret_cast<cudaStream_t>(stream)),
+                     "ray geometry launch");
+}
+
+dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const float aabb_min[3],
+                                       const float aabb_max[3], int32_t res,
+                                       const dmv3d_render_opts *opts, float *t_k, float *points,
+                                       int32_t *texel, float *frac, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_cams(cams)) != DMV3D_OK) return s;
+  CHECK_ARG(aabb_min && aabb_max, "aabb is NULL");
+  CHECK_ARG(res >= 2, "res must be >= 2");
+  if ((s = check_aabb(aabb_min, aabb_max)) != DMV3D_OK) return s;
+  if ((s = check_opts(opts, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
+    return s;
+  dmv3d_triplane t{};
+  t.res = res;
+  t.channels = 4;
+  for (int a = 0; a < 3; ++a) {
+    t.aabb_min[a] = aabb_min[a];
+    t.aabb_max[a] = aabb_max[a];
+  }
+  RenderParams P;
+  fill_common(P, &t, cams, nullptr, opts);
+  return cuda_status(launch_sample_points(P, t_k, points, texel, frac,
+                                          reinterpret_cast<cudaStream_t>(stream)),
+                     "sample points launch");
+}
+
+static dmv3d_cameras no_cams() {
+  dmv3d_cameras c{};
+  c.num_views = c.height = c.width = 1;
+  return c;
+}
+
+dmv3d_status dmv3d_debug_sample_features(const dmv3d_triplane *triplane, dmv3d_agg agg,
+                                         int64_t n, const float *points, float *feats,
+                                         dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
+  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  CHECK_ARG(n >= 0, "n must be >= 0");
+  CHECK_ARG(n == 0 || (points && feats), "points / feats is NULL");
+  if (n) {
+    CHECK_ALIGN(points, "points");
+    CHECK_ALIGN(feats, "feats");
+  }
+  const dmv3d_cameras c = no_cams();
+  RenderParams P;
+  fill_common(P, triplane, &c, nullptr, nullptr);
+  P.agg = agg;
+  cudaError_t e = launch_features(P, triplane->dtype == DMV3D_BF16, n, points, feats,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorInvalidValue)
+    return fail(DMV3D_ERR_UNSUPPORTED, "features: unsupported channel count");
+  return cuda_status(e, "features launch");
+}
+
+dmv3d_status dmv3d_debug_decode(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                dmv3d_agg agg, int64_t n, const float *points, float *sigma_rgb,
+                                dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
+  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
+  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  CHECK_ARG(n >= 0, "n must be >= 0");
+  CHECK_ARG(n == 0 || (points && sigma_rgb), "points / sigma_rgb is NULL");
+  if (n) {
+    CHECK_ALIGN(points, "points");
+    CHECK_ALIGN(sigma_rgb, "sigma_rgb");
+  }
+  if (!simt_supported(mlp->in_dim, mlp->hidden))
+    return fail(DMV3D_ERR_UNSUPPORTED, "decode: unsupported (in_dim, hidden)");
+  const dmv3d_cameras c = no_cams();
+  RenderParams P;
+  fill_common(P, triplane, &c, mlp, nullptr);
+  P.agg = agg;
+  return cuda_status(launch_decode(P, triplane->dtype == DMV3D_BF16, mlp->dtype == DMV3D_BF16, n,
+                                   points, sigma_rgb, reinterpret_cast<cudaStream_t>(stream)),
+                     "decode launch");
+}
+
+// ------------------------------------------------------ host-buffer variant
+struct dmv3d_workspace {
+  struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+  };
+  Buf tp, intr, c2w, xt, z, xp, rgb, alpha, w[kMaxLayers], b[kMaxLayers];
+};
+
+static cudaError_t ws_reserve(dmv3d_workspace::Buf &b, size_t bytes) {
+  if (bytes <= b.cap) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e == cudaSuccess) b.cap = bytes;
+  return e;
+}
+
+dmv3d_status dmv3d_workspace_create(dmv3d_workspace **ws) {
+  g_err.clear();
+  CHECK_ARG(ws != nullptr, "ws is NULL");
+  *ws = new dmv3d_workspace();
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws) {
+  g_err.clear();
+  if (!ws) return DMV3D_OK;
+  dmv3d_workspace::Buf *all[] = {&ws->tp, &ws->intr, &ws->c2w, &ws->xt, &ws->z,
+                                 &ws->xp, &ws->rgb, &ws->alpha};
+  for (auto *b : all)
+    if (b->p) cudaFree(b->p);
+  for (int l = 0; l < kMaxLayers; ++l) {
+    if (ws->w[l].p) cudaFree(ws->w[l].p);
+    if (ws->b[l].p) cudaFree(ws->b[l].p);
+  }
+  delete ws;
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_triplane *triplane,
+                                         const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                         const dmv3d_render_opts *opts,
+                                         const dmv3d_ddim_params *ddim, const float *x_t,
+                                         const float *z, float *x_prev, float *rgb, float *alpha,
+                                         dmv3d_stream stream) {
+  g_err.clear();
+  CHECK_ARG(ws != nullptr, "ws is NULL");
+  CHECK_ARG(triplane && cams && mlp && opts && ddim, "NULL argument");
+  CHECK_ARG(triplane->data && cams->intrinsics && cams->c2w && x_t && x_prev, "NULL host buffer");
+  CHECK_ARG(mlp->num_layers >= 2 && mlp->num_layers <= kMaxLayers, "mlp: num_layers must be in [2, 8]");
+  CHECK_ARG(mlp->weights && mlp->biases, "mlp: weights / biases array is NULL");
+  CHECK_ARG(cams->num_views >= 1 && cams->height >= 1 && cams->width >= 1, "cameras: V, H, W must be >= 1");
+  CHECK_ARG(ddim->ddim_views >= 1 && ddim->ddim_views <= cams->num_views, "ddim: need 1 <= ddim_views <= V");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t V = cams->num_views, HW = (size_t)cams->height * cams->width;
+  const size_t tp_bytes = (size_t)3 * triplane->res * triplane->res * triplane->channels *
+                          (triplane->dtype == DMV3D_BF16 ? 2 : 4);
+  const size_t img_in = (size_t)ddim->ddim_views * 3 * HW * 4;
+  cudaError_t e = cudaSuccess;
+#define TRY(x)                                                  \
+  do {                                                          \
+    e = (x);                                                    \
+    if (e != cudaSuccess) return cuda_status(e, "host step");   \
+  } while (0)
+  TRY(ws_reserve(ws->tp, tp_bytes));
+  TRY(ws_reserve(ws->intr, V * 16));
+  TRY(ws_reserve(ws->c2w, V * 48));
+  TRY(ws_reserve(ws->xt, img_in));
+  TRY(ws_reserve(ws->xp, img_in));
+  if (z) TRY(ws_reserve(ws->z, img_in));
+  if (rgb) TRY(ws_reserve(ws->rgb, V * 3 * HW * 4));
+  if (alpha) TRY(ws_reserve(ws->alpha, V * HW * 4));
+  TRY(cudaMemcpyAsync(ws->tp.p, triplane->data, tp_bytes, cudaMemcpyHostToDevice, st));
+  TRY(cudaMemcpyAsync(ws->intr.p, cams->intrinsics, V * 16, cudaMemcpyHostToDevice, st));
+  TRY(cudaMemcpyAsync(ws->c2w.p, cams->c2w, V * 48, cudaMemcpyHostToDevice, st));
+  TRY(cudaMemcpyAsync(ws->xt.p, x_t, img_in, cudaMemcpyHostToDevice, st));
+  if (z) TRY(cudaMemcpyAsync(ws->z.p, z, img_in, cudaMemcpyHostToDevice, st));
+  const void *dw[kMaxLayers];
+  const float *db[kMaxLayers];
+  const size_t wel = mlp->dtype == DMV3D_BF16 ? 2 : 4;
+  for (int l = 0; l < mlp->num_layers; ++l) {
+    const size_t in = l == 0 ? mlp->in_dim : mlp->hidden;
+    const size_t out = l == mlp->num_layers - 1 ? 4 : mlp->hidden;
+    CHECK_ARG(mlp->weights[l] && mlp->biases[l], "mlp: a layer pointer is NULL");
+    TRY(ws_reserve(ws->w[l], in * out * wel));
+    TRY(ws_reserve(ws->b[l], out * 4));
+    TRY(cudaMemcpyAsync(ws->w[l].p, mlp->weights[l], in * out * wel, cudaMemcpyHostToDevice, st));
+    TRY(cudaMemcpyAsync(ws->b[l].p, mlp->biases[l], out * 4, cudaMemcpyHostToDevice, st));
+    dw[l] = ws->w[l].p;
+    db[l] = static_cast<const float *>(ws->b[l].p);
+  }
+  dmv3d_triplane t = *triplane;
+  t.data = ws->tp.p;
+  dmv3d_cameras c = *cams;
+  c.intrinsics = static_cast<const float *>(ws->intr.p);
+  c.c2w = static_cast<const float *>(ws->c2w.p);
+  dmv3d_mlp m = *mlp;
+  m.weights = dw;
+  m.biases = db;
+  dmv3d_status s = render_impl(&t, &c, &m, opts, ddim, static_cast<const float *>(ws->xt.p),
+                               z ? static_cast<const float *>(ws->z.p) : nullptr,
+                               static_cast<float *>(ws->xp.p),
+                               rgb ? static_cast<float *>(ws->rgb.p) : nullptr,
+                               alpha ? static_cast<float *>(ws->alpha.p) : nullptr, st);
+  if (s != DMV3D_OK) return s;
+  TRY(cudaMemcpyAsync(x_prev, ws->xp.p, img_in, cudaMemcpyDeviceToHost, st));
+  if (rgb) TRY(cudaMemcpyAsync(rgb, ws->rgb.p, V * 3 * HW * 4, cudaMemcpyDeviceToHost, st));
+  if (alpha) TRY(cudaMemcpyAsync(alpha, ws->alpha.p, V * HW * 4, cudaMemcpyDeviceToHost, st));
+#undef TRY
+  return DMV3D_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+// common.cuh -- device-side building blocks shared by the libdmv3d kernels.
+//
+// Geometry (rows a1-a3 of SURVEY.md §8) is computed with explicit IEEE
+// round-to-nearest intrinsics, one rounding per operation and no FMA
+// contraction, so the integer/geometry outputs are bit-identical to any
+// implementation that follows the same operation order (DESIGN.md
+// "Bit-exact geometry").  Everything after the texel indices is ordinary
+// fp32 (or bf16 tensor-core) arithmetic.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dmv3d {
+
+constexpr int kMaxLayers = 8;
+
+// All per-launch parameters; passed by value as a __grid_constant__.
+struct RenderParams {
+  // camera set C
+  int32_t V, H, W;
+  const float *intr;  // [V][4]
+  const float *c2w;   // [V][3][4]
+  // triplane S
+  int32_t R, C;
+  const void *tp;  // [3][R][R][C]
+  float lo[3], hi[3];
+  // shared MLP
+  int32_t L, K, HD;
+  const void *w[kMaxLayers];
+  const float *b[kMaxLayers];
+  int32_t act;
+  float dshift, weps;
+  // ray marching
+  int32_t N, agg, jitter;
+  uint64_t seed;
+  float bg[3];
+  float term_eps;
+  int64_t ray_begin, ray_end;
+  // outputs
+  float *rgb;    // [V][3][H][W] or null
+  float *alpha;  // [V][H][W] or null
+  // fused DDIM epilogue, views [0, ddim_views)
+  int32_t ddim_views;
+  uint64_t keep_bits;
+  const float *x_t, *z;
+  float *x_prev;
+  float x0_scale, x0_shift;
+  float sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
+  unsigned long long *counters;
+};
+
+// ---------------------------------------------------------------- a1: rays
+// Pinhole camera, pixel centre at +1/2, OpenCV axes, unit direction.
+struct Ray {
+  float o[3], d[3];
+  float t_near, t_far;
+  bool hit;
+};
+
+__device__ __forceinline__ void ray_pixel(int64_t r, int H, int W, int &v, int &i, int &j) {
+  const int64_t HW = (int64_t)H * W;
+  const int64_t vv = r / HW;
+  const int64_t rem = r - vv * HW;
+  const int64_t ii = rem / W;
+  v = (int)vv;
+  i = (int)ii;
+  j = (int)(rem - ii * W);
+}
+
+__device__ __forceinline__ Ray make_ray(const float *__restrict__ intr,
+                                        const float *__restrict__ c2w, int v, int i, int j,
+                                        const float lo[3], const float hi[3]) {
+  Ray ray;
+  const float *K = intr + 4 * v;
+  const float *M = c2w + 12 * v;
+  const float xc = __fdiv_rn(__fsub_rn(__fadd_rn(__int2float_rn(j), 0.5f), __ldg(K + 2)),
+                             __ldg(K + 0));
+  const float yc = __fdiv_rn(__fsub_rn(__fadd_rn(__int2float_rn(i), 0.5f), __ldg(K + 3)),
+                             __ldg(K + 1));
+  float dw[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float s = __fadd_rn(__fmul_rn(__ldg(M + 4 * a + 0), xc), __fmul_rn(__ldg(M + 4 * a + 1), yc));
+    dw[a] = __fadd_rn(s, __ldg(M + 4 * a + 2));
+  }
+  const float nn = __fadd_rn(__fadd_rn(__fmul_rn(dw[0], dw[0]), __fmul_rn(dw[1], dw[1])),
+                             __fmul_rn(dw[2], dw[2]));
+  const float n = __fsqrt_rn(nn);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ray.d[a] = __fdiv_rn(dw[a], n);
+    ray.o[a] = __ldg(M + 4 * a + 3);
+  }
+  // a2: slab test against [lo, hi] (reading A9)
+  bool ok = true;
+  float tmin[3], tmax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (ray.d[a] == 0.0f) {
+      ok = ok && !(ray.o[a] < lo[a] || ray.o[a] > hi[a]);
+      tmin[a] = -INFINITY;
+      tmax[a] = INFINITY;
+    } else {
+      const float t0 = __fdiv_rn(__fsub_rn(lo[a], ray.o[a]), ray.d[a]);
+      const float t1 = __fdiv_rn(__fsub_rn(hi[a], ray.o[a]), ray.d[a]);
+      tmin[a] = fminf(t0, t1);
+      tmax[a] = fmaxf(t0, t1);
+    }
+  }
+  const float tn = fmaxf(fmaxf(fmaxf(tmin[0], tmin[1]), tmin[2]), 0.0f);
+  const float tf = fminf(fminf(tmax[0], tmax[1]), tmax[2]);
+  ray.hit = ok && (tf > tn);
+  ray.t_near = ray.hit ? tn : 0.0f;
+  ray.t_far = ray.hit ? tf : 0.0f;
+  return ray;
+}
+
+// ------------------------------------------------------------- a2: samples
+// Reading A10: optional stratified jitter, splitmix64 finaliser on the
+// sample id (portable counter-based generator).
+__device__ __forceinline__ float jitter_u(uint64_t seed, uint64_t sample_id) {
+  uint64_t z = seed + (sample_id + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  return __fmul_rn(__uint2float_rn((uint32_t)(z >> 40)), 1.0f / 16777216.0f);
+}
+
+__device__ __forceinline__ float sample_delta(const Ray &ray, int N) {
+  return __fdiv_rn(__fsub_rn(ray.t_far, ray.t_near), __int2float_rn(N));
+}
+
+__device__ __forceinline__ float sample_t(const Ray &ray, float delta, int k, float u) {
+  return __fadd_rn(ray.t_near, __fmul_rn(__fadd_rn(__int2float_rn(k), u), delta));
+}
+
+__device__ __forceinline__ void sample_p(const Ray &ray, float t, float p[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) p[a] = __fadd_rn(ray.o[a], __fmul_rn(t, ray.d[a]));
+}
+
+// ------------------------------------------------------------ a3: texels
+// Reading A3: align-corners, clamped; i0 in [0, R-2], f in [0, 1].
+__device__ __forceinline__ void texel_coord(float q, float lo, float hi, int R, int &i0,
+                                            float &f) {
+  const float s = __fdiv_rn(__fsub_rn(q, lo), __fsub_rn(hi, lo));
+  float px = __fmul_rn(s, __int2float_rn(R - 1));
+  px = fminf(fmaxf(px, 0.0f), __int2float_rn(R - 1));
+  int ix = __float2int_rd(px);
+  ix = min(ix, R - 2);
+  i0 = ix;
+  f = __fsub_rn(px, __int2float_rn(ix));
+}
+
+// Plane (a, b) for planes XY, XZ, YZ (reading A2).
+__device__ __forceinline__ int plane_axis_a(int pl) { return pl == 2 ? 1 : 0; }
+__device__ __forceinline__ int plane_axis_b(int pl) { return pl == 0 ? 1 : 2; }
+
+// One plane's bilinear cell: element offset of texel (iy, ix) and fractions.
+struct Cell {
+  int64_t off;  // element offset of corner (iy, ix) of plane pl
+  float fx, fy;
+};
+
+__device__ __forceinline__ Cell plane_cell(const float p[3], int pl, int R, int C,
+                                           const float lo[3], const float hi[3]) {
+  const int a = plane_axis_a(pl), b = plane_axis_b(pl);
+  int ix, iy;
+  float fx, fy;
+  texel_coord(p[a], lo[a], hi[a], R, ix, fx);
+  texel_coord(p[b], lo[b], hi[b], R, iy, fy);
+  Cell c;
+  c.off = (((int64_t)pl * R + iy) * R + ix) * C;
+  c.fx = fx;
+  c.fy = fy;
+  return c;
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ float softplus_f(float x) {
+  return log1pf(expf(-fabsf(x))) + fmaxf(x, 0.0f);
+}
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf(-x)); }
+__device__ __forceinline__ float hidden_act_f(int kind, float x) {
+  if (kind == 1) return x * sigmoid_f(x);
+  if (kind == 2) return softplus_f(x);
+  return fmaxf(x, 0.0f);
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+// Per-ray epilogue: write rgb/alpha and, for DDIM views, x_{t-1}
+// (readings A15, A18-A20).  `ch` selects the channel this
+// thread writes (0..2); channel 0's thread also writes alpha.
+__device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i, int j, int ch,
+                                             float c_val, float T) {
+  const int64_t HW = (int64_t)P.H * P.W;
+  const int64_t pix = (int64_t)i * P.W + j;
+  const float out = c_val + T * P.bg[ch];
+  if (P.rgb) P.rgb[((int64_t)v * 3 + ch) * HW + pix] = out;
+  if (ch == 0 && P.alpha) P.alpha[(int64_t)v * HW + pix] = 1.0f - T;
+  if (v < P.ddim_views) {
+    const int64_t idx = ((int64_t)v * 3 + ch) * HW + pix;
+    const float xt = __ldg(P.x_t + idx);
+    float xp;
+    if ((P.keep_bits >> v) & 1ull) {
+      xp = xt;
+    } else {
+      const float x0 = P.x0_scale * out + P.x0_shift;
+      const float eps = (xt - P.sqrt_ab_t * x0) * P.inv_sqrt_1m_ab_t;
+      xp = P.sqrt_ab_p * x0 + P.c_eps * eps;
+      if (P.sigma_t != 0.0f) xp += P.sigma_t * __ldg(P.z + idx);
+    }
+    P.x_prev[idx] = xp;
+  }
+}
+
+}  // namespace dmv3d

@@ -1,0 +1,170 @@
+// elementwise.cu -- standalone DDIM step (row a6) and the stage-level debug
+// kernels for rows a1-a3 (bit-exact geometry dumps).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dmv3d {
+
+// ------------------------------------------------------------------ a6
+// x0 = s*rgb + b; eps = (x_t - sqrt(ab_t) x0) / sqrt(1 - ab_t);
+// x_{t-1} = sqrt(ab_p) x0 + c_eps eps + sigma_t z
+__device__ __forceinline__ float ddim_one(const DdimCoef &c, float xt, float rgb, float z) {
+  const float x0 = c.x0_scale * rgb + c.x0_shift;
+  const float eps = (xt - c.sqrt_ab_t * x0) * c.inv_sqrt_1m_ab_t;
+  float xp = c.sqrt_ab_p * x0 + c.c_eps * eps;
+  if (c.sigma_t != 0.0f) xp += c.sigma_t * z;
+  return xp;
+}
+
+// HBM-bound: 16-byte loads/stores, grid = multiple of the SM count.
+__global__ void ddim_kernel(const __grid_constant__ DdimCoef c, int64_t per_view, int64_t n4,
+                            const float4 *__restrict__ x_t, const float4 *__restrict__ x0,
+                            const float4 *__restrict__ z, float4 *__restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)((q * 4) / per_view);
+    const float4 xt = __ldg(x_t + q);
+    if ((c.keep_bits >> v) & 1ull) {
+      out[q] = xt;
+      continue;
+    }
+    const float4 r = __ldg(x0 + q);
+    const float4 zz = (c.sigma_t != 0.0f) ? __ldg(z + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 o;
+    o.x = ddim_one(c, xt.x, r.x, zz.x);
+    o.y = ddim_one(c, xt.y, r.y, zz.y);
+    o.z = ddim_one(c, xt.z, r.z, zz.z);
+    o.w = ddim_one(c, xt.w, r.w, zz.w);
+    out[q] = o;
+  }
+}
+
+__global__ void ddim_kernel_scalar(const __grid_constant__ DdimCoef c, int64_t per_view,
+                                   int64_t n, const float *__restrict__ x_t,
+                                   const float *__restrict__ x0, const float *__restrict__ z,
+                                   float *__restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(q / per_view);
+    const float xt = x_t[q];
+    out[q] = ((c.keep_bits >> v) & 1ull) ? xt
+                                          : ddim_one(c, xt, x0[q], c.sigma_t != 0.0f ? z[q] : 0.0f);
+  }
+}
+
+static int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+cudaError_t launch_ddim(const DdimCoef &c, int V, int H, int W, const float *x_t,
+                        const float *x0_rgb, const float *z, const uint8_t *, float *x_prev,
+                        cudaStream_t st) {
+  const int64_t per_view = (int64_t)3 * H * W;
+  const int64_t n = per_view * V;
+  if (n == 0) return cudaSuccess;
+  const int threads = 256;
+  if (per_view % 4 == 0) {
+    const int64_t n4 = n / 4;
+    int64_t grid = (n4 + threads - 1) / threads;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    ddim_kernel<<<(int)grid, threads, 0, st>>>(c, per_view, n4,
+                                               reinterpret_cast<const float4 *>(x_t),
+                                               reinterpret_cast<const float4 *>(x0_rgb),
+                                               reinterpret_cast<const float4 *>(z),
+                                               reinterpret_cast<float4 *>(x_prev));
+  } else {
+    int64_t grid = (n + threads - 1) / threads;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    ddim_kernel_scalar<<<(int)grid, threads, 0, st>>>(c, per_view, n, x_t, x0_rgb, z, x_prev);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- a1-a3 debug dumps
+__global__ void ray_geometry_kernel(const __grid_constant__ RenderParams P, float *o_d,
+                                    float *tn_tf, uint8_t *hit) {
+  const int64_t n = P.ray_end - P.ray_begin;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int v, i, j;
+    ray_pixel(P.ray_begin + q, P.H, P.W, v, i, j);
+    const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    if (o_d) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        o_d[6 * q + a] = ray.o[a];
+        o_d[6 * q + 3 + a] = ray.d[a];
+      }
+    }
+    if (tn_tf) {
+      tn_tf[2 * q] = ray.t_near;
+      tn_tf[2 * q + 1] = ray.t_far;
+    }
+    if (hit) hit[q] = ray.hit ? 1 : 0;
+  }
+}
+
+__global__ void sample_points_kernel(const __grid_constant__ RenderParams P, float *t_k,
+                                     float *points, int32_t *texel, float *frac) {
+  const int64_t n = (P.ray_end - P.ray_begin) * P.N;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = q / P.N;
+    const int k = (int)(q - rr * P.N);
+    const int64_t r = P.ray_begin + rr;
+    int v, i, j;
+    ray_pixel(r, P.H, P.W, v, i, j);
+    const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    float t = 0.0f, p[3] = {0.0f, 0.0f, 0.0f};
+    int idx[6] = {0, 0, 0, 0, 0, 0};
+    float fr[6] = {0, 0, 0, 0, 0, 0};
+    if (ray.hit) {
+      const float delta = sample_delta(ray, P.N);
+      const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
+      t = sample_t(ray, delta, k, u);
+      sample_p(ray, t, p);
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl) {
+        const int a = plane_axis_a(pl), b = plane_axis_b(pl);
+        texel_coord(p[a], P.lo[a], P.hi[a], P.R, idx[2 * pl], fr[2 * pl]);
+        texel_coord(p[b], P.lo[b], P.hi[b], P.R, idx[2 * pl + 1], fr[2 * pl + 1]);
+      }
+    }
+    if (t_k) t_k[q] = t;
+    if (points) {
+      points[3 * q] = p[0];
+      points[3 * q + 1] = p[1];
+      points[3 * q + 2] = p[2];
+    }
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      if (texel) texel[6 * q + e] = idx[e];
+      if (frac) frac[6 * q + e] = fr[e];
+    }
+  }
+}
+
+cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
+                                cudaStream_t st) {
+  const int64_t n = P.ray_end - P.ray_begin;
+  if (n <= 0) return cudaSuccess;
+  const int64_t grid = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+  ray_geometry_kernel<<<(int)grid, 256, 0, st>>>(P, o_d, tn_tf, hit);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_points(const RenderParams &P, float *t_k, float *points,
+                                 int32_t *texel, float *frac, cudaStream_t st) {
+  const int64_t n = (P.ray_end - P.ray_begin) * P.N;
+  if (n <= 0) return cudaSuccess;
+  const int64_t grid = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  sample_points_kernel<<<(int)grid, 256, 0, st>>>(P, t_k, points, texel, frac);
+  return cudaGetLastError();
+}
+
+}  // namespace dmv3d

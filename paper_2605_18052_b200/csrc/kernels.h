@@ -1,0 +1,38 @@
+// kernels.h -- internal launchers of libdmv3d (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace dmv3d {
+
+constexpr int kSimtThreads = 128;
+
+// render_simt.cu
+bool simt_supported(int K, int HD);
+size_t simt_smem_bytes(int K, int HD, int L);
+cudaError_t launch_render_simt(const RenderParams &P, bool tp_bf16, bool w_bf16,
+                               cudaStream_t st);
+cudaError_t launch_features(const RenderParams &P, bool tp_bf16, int64_t n, const float *pts,
+                            float *out, cudaStream_t st);
+cudaError_t launch_decode(const RenderParams &P, bool tp_bf16, bool w_bf16, int64_t n,
+                          const float *pts, float *out, cudaStream_t st);
+
+// render_tc.cu (tcgen05 / TMEM engine)
+bool tc_supported(int K, int HD, int L);
+cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
+
+// elementwise.cu
+struct DdimCoef {
+  float x0_scale, x0_shift, sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
+  uint64_t keep_bits;
+};
+cudaError_t launch_ddim(const DdimCoef &c, int V, int H, int W, const float *x_t,
+                        const float *x0_rgb, const float *z, const uint8_t *keep_dev,
+                        float *x_prev, cudaStream_t st);
+cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
+                                cudaStream_t st);
+cudaError_t launch_sample_points(const RenderParams &P, float *t_k, float *points,
+                                 int32_t *texel, float *frac, cudaStream_t st);
+
+}  // namespace dmv3d

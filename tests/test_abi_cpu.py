@@ -1,0 +1,122 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports
+every symbol include/dmv3d.h declares, and rejects bad arguments with the
+documented status before touching the device."""
+import ctypes as ct
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2605_18052_b200 import _abi, schedule
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "dmv3d.h")).read()
+    return sorted(set(re.findall(r"\b(dmv3d_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _abi.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(_abi.EXPORTED) <= set(syms)
+    assert b"sm_100a" in L.dmv3d_version()
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_abi.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def _valid_structs(keep):
+    intr = np.zeros((1, 4), np.float32)
+    c2w = np.zeros((1, 3, 4), np.float32)
+    tp = np.zeros((3, 4, 4, 8), np.float32)
+    keep += [intr, c2w, tp]
+    cams = _abi.Cameras(1, 4, 4, intr.ctypes.data, c2w.ctypes.data)
+    t = _abi.Triplane(4, 8, _abi.F32, tp.ctypes.data, (ct.c_float * 3)(-1, -1, -1),
+                      (ct.c_float * 3)(1, 1, 1))
+    ws = [np.zeros((16, 8), np.float32), np.zeros((4, 16), np.float32)]
+    bs = [np.zeros(16, np.float32), np.zeros(4, np.float32)]
+    keep += ws + bs
+    warr = (ct.c_void_p * 2)(*[w.ctypes.data for w in ws])
+    barr = (ct.c_void_p * 2)(*[b.ctypes.data for b in bs])
+    keep += [warr, barr]
+    m = _abi.MLP(2, 8, 16, _abi.F32, ct.cast(warr, ct.POINTER(ct.c_void_p)),
+                 ct.cast(barr, ct.POINTER(ct.c_void_p)), 0, 0.0, 0.0)
+    o = _abi.RenderOpts(16, 0, 0, 0, (ct.c_float * 3)(1, 1, 1), 0.0, -1, -1, 0, None)
+    return t, cams, m, o
+
+
+@pytest.mark.parametrize("mutate,status", [
+    (lambda t, c, m, o: setattr(c, "num_views", 0), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(t, "res", 1), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(t, "channels", 6), _abi.ERR_UNSUPPORTED),
+    (lambda t, c, m, o: setattr(m, "num_layers", 1), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(m, "num_layers", 9), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(m, "in_dim", 4), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(o, "samples_per_ray", 0), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(o, "samples_per_ray", 1025), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(o, "term_eps", 1.5), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: (setattr(o, "ray_begin", 5), setattr(o, "ray_end", 4)), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: (setattr(o, "ray_begin", 0), setattr(o, "ray_end", 17)), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(t, "data", t.data + 4), _abi.ERR_ALIGNMENT),
+    (lambda t, c, m, o: setattr(c, "c2w", c.c2w + 8), _abi.ERR_ALIGNMENT),
+    (lambda t, c, m, o: setattr(o, "engine", _abi.ENGINE_TCGEN05), _abi.ERR_UNSUPPORTED),
+    (lambda t, c, m, o: setattr(m, "hidden", 17), _abi.ERR_UNSUPPORTED),
+])
+def test_render_argument_validation(mutate, status):
+    keep = []
+    t, c, m, o = _valid_structs(keep)
+    mutate(t, c, m, o)
+    rgb = np.zeros(64, np.float32)
+    st = _abi.lib().dmv3d_render_views(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o),
+                                       rgb.ctypes.data, None, None)
+    assert st == status, _abi.lib().dmv3d_last_error()
+    assert len(_abi.lib().dmv3d_last_error()) > 0
+
+
+def test_render_null_rgb_rejected():
+    keep = []
+    t, c, m, o = _valid_structs(keep)
+    st = _abi.lib().dmv3d_render_views(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o), None,
+                                       None, None)
+    assert st == _abi.ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("field,value", [("t", 1000), ("t", -1), ("t_prev", 980), ("eta", 1.5)])
+def test_ddim_argument_validation(field, value):
+    ab = schedule.cosine_alpha_bar()
+    d = _abi.DdimParams(ab.ctypes.data_as(ct.POINTER(ct.c_double)), 1000, 980, 960, 0.0, 2.0, -1.0,
+                        None, 1)
+    setattr(d, field, value)
+    x = np.zeros(48, np.float32)
+    st = _abi.lib().dmv3d_ddim_step(ct.byref(d), 1, 4, 4, x.ctypes.data, x.ctypes.data, None,
+                                    x.ctypes.data, None)
+    assert st == _abi.ERR_INVALID_ARG
+
+
+def test_ddim_eta_needs_z():
+    ab = schedule.cosine_alpha_bar()
+    d = _abi.DdimParams(ab.ctypes.data_as(ct.POINTER(ct.c_double)), 1000, 980, 960, 0.5, 2.0, -1.0,
+                        None, 1)
+    x = np.zeros(48, np.float32)
+    st = _abi.lib().dmv3d_ddim_step(ct.byref(d), 1, 4, 4, x.ctypes.data, x.ctypes.data, None,
+                                    x.ctypes.data, None)
+    assert st == _abi.ERR_INVALID_ARG
+    assert b"z" in _abi.lib().dmv3d_last_error()
+
+
+def test_product_schedule_matches_oracle():
+    """Host logic: the product's alpha_bar table equals the (pinned) oracle's."""
+    assert np.max(np.abs(schedule.cosine_alpha_bar() - oracle.cosine_alpha_bar())) < 1e-14
+    ts = schedule.ddim_timesteps()
+    assert ts[0] == 980 and ts[-1] == 0 and len(ts) == 50
+    assert schedule.ddim_pairs()[-1] == (0, -1)
