@@ -99,7 +99,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_rate(w, budget_s: float, threads: int, max_rays: int = 65536, seed: int = 7):
+def oracle_rate(w, budget_s: float, threads: int, max_rays: int = 524288, seed: int = 7):
     """Oracle rays/s on a bounded random sample of the workload's rays."""
     import oracle
     rng = np.random.default_rng(seed)

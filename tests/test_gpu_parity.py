@@ -118,7 +118,7 @@ def test_decode_matches_oracle(C, H, L, act):
     want = oracle.decode_points(tp, m, pts)
     err = np.abs(g - want)
     assert np.max(err[:, 1:]) < FP32_TOL
-    assert np.max(err[:, 0] / np.maximum(1.0, want[:, 0])) < 2e-6
+    assert np.max(err[:, 0] / np.maximum(1.0, want[:, 0])) < 1e-5  # ~K*eps_f32 over 3 layers
 
 
 # ------------------------------------------------------------------ a1-a5 render
