@@ -64,7 +64,9 @@ typedef enum { DMV3D_ACT_RELU = 0, DMV3D_ACT_SILU = 1, DMV3D_ACT_SOFTPLUS = 2 } 
 typedef enum {
   DMV3D_ENGINE_AUTO = 0,   /* tensor cores when the shapes allow, else SIMT            */
   DMV3D_ENGINE_SIMT = 1,   /* fp32 CUDA-core MLP (fp32 or bf16 storage)                */
-  DMV3D_ENGINE_TCGEN05 = 2 /* bf16 tcgen05/TMEM MLP, fp32 accumulation (bf16 only)     */
+  DMV3D_ENGINE_TCGEN05 = 2 /* tensor cores: bf16 storage, blend + MLP as fp16 tcgen05
+                              MMAs with fp32 TMEM accumulation; ReLU, hidden 64, needs
+                              opts.workspace; |values| must stay below 65504 (fp16)     */
 } dmv3d_engine;
 
 /* Camera set C ("viewpoints C = {c_1..c_N}"). */
@@ -110,7 +112,16 @@ typedef struct {
   unsigned long long *counters; /* optional DEVICE [4] accumulators (NULL = off):
                               [0] rays hit, [1] samples evaluated,
                               [2] rays terminated early, [3] rays processed           */
+  void *workspace;         /* DEVICE scratch of >= dmv3d_workspace_bytes() bytes, 256-B
+                              aligned; required by the TCGEN05 engine (holds the
+                              per-step projected triplane), ignored by SIMT.  One
+                              workspace per stream: calls sharing it must be ordered. */
+  uint64_t workspace_bytes;
 } dmv3d_render_opts;
+
+/* Scratch the TCGEN05 engine needs for this triplane/MLP (0 if it cannot run
+ * them): 256 + 3*R*R*hidden*2 bytes. */
+uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp);
 
 /* DDIM x0 -> x_{t-1} (readings A15-A20). */
 typedef struct {

@@ -21,7 +21,7 @@ EXPORTED = [
     "dmv3d_render_views", "dmv3d_ddim_step", "dmv3d_render_ddim_step", "dmv3d_last_error",
     "dmv3d_version", "dmv3d_workspace_create", "dmv3d_workspace_destroy",
     "dmv3d_render_ddim_step_host", "dmv3d_debug_ray_geometry", "dmv3d_debug_sample_points",
-    "dmv3d_debug_sample_features", "dmv3d_debug_decode",
+    "dmv3d_debug_sample_features", "dmv3d_debug_decode", "dmv3d_workspace_bytes",
 ]
 
 
@@ -46,7 +46,8 @@ class RenderOpts(ct.Structure):
     _fields_ = [("samples_per_ray", ct.c_int32), ("agg", ct.c_int32), ("jitter", ct.c_int32),
                 ("seed", ct.c_uint64), ("bg_rgb", ct.c_float * 3), ("term_eps", ct.c_float),
                 ("ray_begin", ct.c_int64), ("ray_end", ct.c_int64), ("engine", ct.c_int32),
-                ("counters", ct.c_void_p)]
+                ("counters", ct.c_void_p), ("workspace", ct.c_void_p),
+                ("workspace_bytes", ct.c_uint64)]
 
 
 class DdimParams(ct.Structure):
@@ -100,8 +101,10 @@ def lib() -> ct.CDLL:
                                                   ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_debug_decode.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int64,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
+        L.dmv3d_workspace_bytes.argtypes = [P(Triplane), P(MLP)]
+        L.dmv3d_workspace_bytes.restype = ct.c_uint64
         for name in EXPORTED:
-            if name not in ("dmv3d_last_error", "dmv3d_version"):
+            if name not in ("dmv3d_last_error", "dmv3d_version", "dmv3d_workspace_bytes"):
                 getattr(L, name).restype = ct.c_int
         _lib = L
     return _lib

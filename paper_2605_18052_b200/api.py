@@ -70,11 +70,30 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
-                term_eps=0.0, ray_range=None, engine="auto", counters=None):
+                term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None):
     b, e = (-1, -1) if ray_range is None else ray_range
+    ws_ptr = None if workspace is None else workspace.data_ptr()
+    ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
     return _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
                            (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
-                           None if counters is None else counters.data_ptr())
+                           None if counters is None else counters.data_ptr(), ws_ptr, ws_len)
+
+
+_WS_CACHE = {}
+
+
+def workspace_for(triplane_s, mlp_s, device, stream=None):
+    """Device scratch for the tensor-core engine (dmv3d_workspace_bytes), cached per
+    (device, stream): calls that share a workspace must be ordered on one stream."""
+    n = int(_abi.lib().dmv3d_workspace_bytes(ct.byref(triplane_s), ct.byref(mlp_s)))
+    if n == 0 or device.type != "cuda":
+        return None
+    key = (device.index, None if stream is None else stream.cuda_stream)
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
 
 
 def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mask, ddim_views,
@@ -105,6 +124,8 @@ def dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
     t = triplane_struct(triplane, aabb_min, aabb_max)
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
+    if "workspace" not in opts:
+        opts["workspace"] = workspace_for(t, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(**opts)
     _abi.check(_abi.lib().dmv3d_render_views(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o),
                                              _ptr(rgb), _ptr(alpha), _stream(dev)))
@@ -143,6 +164,8 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
     tt = triplane_struct(triplane, aabb_min, aabb_max)
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
+    if "workspace" not in opts:
+        opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(**opts)
     d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift)
     _abi.check(_abi.lib().dmv3d_render_ddim_step(ct.byref(tt), ct.byref(c), ct.byref(m),

@@ -93,6 +93,8 @@ dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
   CHECK_ARG(all || (o->ray_begin >= 0 && o->ray_begin <= o->ray_end && o->ray_end <= nrays),
             "opts: ray range must be -1,-1 or 0 <= begin <= end <= V*H*W");
   if (o->counters) CHECK_ALIGN(o->counters, "opts.counters");
+  if (o->workspace && (reinterpret_cast<uintptr_t>(o->workspace) & 255u))
+    return fail(DMV3D_ERR_ALIGNMENT, "opts.workspace is not 256-byte aligned");
   return DMV3D_OK;
 }
 
@@ -134,6 +136,8 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.ray_begin = (o->ray_begin == -1 && o->ray_end == -1) ? 0 : o->ray_begin;
     P.ray_end = (o->ray_begin == -1 && o->ray_end == -1) ? nrays : o->ray_end;
     P.counters = o->counters;
+    P.ws = o->workspace;
+    P.ws_bytes = o->workspace_bytes;
   }
 }
 
@@ -172,15 +176,21 @@ enum class Engine { SIMT, TC };
 dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3d_render_opts *o,
                          Engine &e) {
   const bool bf16 = t->dtype == DMV3D_BF16 && m->dtype == DMV3D_BF16;
-  const bool tc_ok = bf16 && tc_supported(m->in_dim, m->hidden, m->num_layers);
+  const bool tc_ok = bf16 && m->hidden_act == DMV3D_ACT_RELU &&
+                     tc_supported(m->in_dim, m->hidden, m->num_layers);
+  const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden);
   if (o->engine == DMV3D_ENGINE_TCGEN05) {
     if (!tc_ok)
       return fail(DMV3D_ERR_UNSUPPORTED,
-                  "engine TCGEN05 needs bf16 triplane + weights and a supported (in_dim, hidden, L)");
+                  "engine TCGEN05 needs bf16 triplane + weights, ReLU, hidden 64, in_dim % 8 == 0 "
+                  "(<= 256), 2 <= L <= 8");
+    if (!ws_ok)
+      return fail(DMV3D_ERR_INVALID_ARG,
+                  "engine TCGEN05 needs opts.workspace of dmv3d_workspace_bytes() bytes");
     e = Engine::TC;
     return DMV3D_OK;
   }
-  if (o->engine == DMV3D_ENGINE_AUTO && tc_ok && m->hidden_act == DMV3D_ACT_RELU) {
+  if (o->engine == DMV3D_ENGINE_AUTO && tc_ok && ws_ok) {
     e = Engine::TC;
     return DMV3D_OK;
   }
@@ -253,7 +263,13 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
 extern "C" {
 
 const char *dmv3d_last_error(void) { return g_err.c_str(); }
-const char *dmv3d_version(void) { return "dmv3d-b200 0.1 (sm_100a)"; }
+const char *dmv3d_version(void) { return "dmv3d-b200 0.2 (sm_100a)"; }
+
+uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp) {
+  if (!triplane || !mlp || triplane->res < 2) return 0;
+  if (!tc_supported(mlp->in_dim, mlp->hidden, mlp->num_layers)) return 0;
+  return tc_workspace_bytes(triplane->res, mlp->hidden);
+}
 
 dmv3d_status dmv3d_render_views(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
                                 const dmv3d_mlp *mlp, const dmv3d_render_opts *opts, float *rgb,
@@ -404,7 +420,7 @@ struct dmv3d_workspace {
     void *p = nullptr;
     size_t cap = 0;
   };
-  Buf tp, intr, c2w, xt, z, xp, rgb, alpha, w[kMaxLayers], b[kMaxLayers];
+  Buf tp, intr, c2w, xt, z, xp, rgb, alpha, scratch, w[kMaxLayers], b[kMaxLayers];
 };
 
 static cudaError_t ws_reserve(dmv3d_workspace::Buf &b, size_t bytes) {
@@ -428,7 +444,7 @@ dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws) {
   g_err.clear();
   if (!ws) return DMV3D_OK;
   dmv3d_workspace::Buf *all[] = {&ws->tp, &ws->intr, &ws->c2w, &ws->xt, &ws->z,
-                                 &ws->xp, &ws->rgb, &ws->alpha};
+                                 &ws->xp, &ws->rgb, &ws->alpha, &ws->scratch};
   for (auto *b : all)
     if (b->p) cudaFree(b->p);
   for (int l = 0; l < kMaxLayers; ++l) {
@@ -499,7 +515,16 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
   dmv3d_mlp m = *mlp;
   m.weights = dw;
   m.biases = db;
-  dmv3d_status s = render_impl(&t, &c, &m, opts, ddim, static_cast<const float *>(ws->xt.p),
+  dmv3d_render_opts o = *opts;
+  if (!o.workspace) {
+    const uint64_t need = dmv3d_workspace_bytes(&t, &m);
+    if (need) {
+      TRY(ws_reserve(ws->scratch, need));
+      o.workspace = ws->scratch.p;
+      o.workspace_bytes = need;
+    }
+  }
+  dmv3d_status s = render_impl(&t, &c, &m, &o, ddim, static_cast<const float *>(ws->xt.p),
                                z ? static_cast<const float *>(ws->z.p) : nullptr,
                                static_cast<float *>(ws->xp.p),
                                rgb ? static_cast<float *>(ws->rgb.p) : nullptr,

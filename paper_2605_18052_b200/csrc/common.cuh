@@ -49,6 +49,9 @@ struct RenderParams {
   float x0_scale, x0_shift;
   float sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
   unsigned long long *counters;
+  // caller-owned scratch (tensor-core engine: patch counter + projected triplane)
+  void *ws;
+  size_t ws_bytes;
 };
 
 // ---------------------------------------------------------------- a1: rays

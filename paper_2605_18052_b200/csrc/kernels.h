@@ -20,6 +20,7 @@ cudaError_t launch_decode(const RenderParams &P, bool tp_bf16, bool w_bf16, int6
 
 // render_tc.cu (tcgen05 / TMEM engine)
 bool tc_supported(int K, int HD, int L);
+size_t tc_workspace_bytes(int R, int HD);
 cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
 
 // elementwise.cu
