@@ -112,6 +112,11 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
   for (int a = 0; a < 3; ++a) {
     P.lo[a] = t->aabb_min[a];
     P.hi[a] = t->aabb_max[a];
+    // exact reciprocal when the extent (as the kernels compute it, in fp32) is 2^k
+    const float ext = P.hi[a] - P.lo[a];
+    int e2 = 0;
+    const float mant = frexpf(ext, &e2);
+    P.inv_ext[a] = (mant == 0.5f && isnormal(ext) && isnormal(1.0f / ext)) ? 1.0f / ext : 0.0f;
   }
   if (m) {
     P.L = m->num_layers;

@@ -26,6 +26,7 @@ struct RenderParams {
   int32_t R, C;
   const void *tp;  // [3][R][R][C]
   float lo[3], hi[3];
+  float inv_ext[3];  // 1/(hi-lo) if a power of two, else 0 (see texel_coord)
   // shared MLP
   int32_t L, K, HD;
   const void *w[kMaxLayers];
@@ -146,9 +147,12 @@ __device__ __forceinline__ void sample_p(const Ray &ray, float t, float p[3]) {
 
 // ------------------------------------------------------------ a3: texels
 // Reading A3: align-corners, clamped; i0 in [0, R-2], f in [0, 1].
-__device__ __forceinline__ void texel_coord(float q, float lo, float hi, int R, int &i0,
-                                            float &f) {
-  const float s = __fdiv_rn(__fsub_rn(q, lo), __fsub_rn(hi, lo));
+// `inv` = 1/(hi - lo) when hi - lo is a power of two (then x/(hi-lo) and
+// x*inv are the same correctly rounded value), else 0 (IEEE division).
+__device__ __forceinline__ void texel_coord(float q, float lo, float hi, float inv, int R,
+                                            int &i0, float &f) {
+  const float num = __fsub_rn(q, lo);
+  const float s = (inv != 0.0f) ? __fmul_rn(num, inv) : __fdiv_rn(num, __fsub_rn(hi, lo));
   float px = __fmul_rn(s, __int2float_rn(R - 1));
   px = fminf(fmaxf(px, 0.0f), __int2float_rn(R - 1));
   int ix = __float2int_rd(px);
@@ -168,12 +172,13 @@ struct Cell {
 };
 
 __device__ __forceinline__ Cell plane_cell(const float p[3], int pl, int R, int C,
-                                           const float lo[3], const float hi[3]) {
+                                           const float lo[3], const float hi[3],
+                                           const float inv[3]) {
   const int a = plane_axis_a(pl), b = plane_axis_b(pl);
   int ix, iy;
   float fx, fy;
-  texel_coord(p[a], lo[a], hi[a], R, ix, fx);
-  texel_coord(p[b], lo[b], hi[b], R, iy, fy);
+  texel_coord(p[a], lo[a], hi[a], inv[a], R, ix, fx);
+  texel_coord(p[b], lo[b], hi[b], inv[b], R, iy, fy);
   Cell c;
   c.off = (((int64_t)pl * R + iy) * R + ix) * C;
   c.fx = fx;

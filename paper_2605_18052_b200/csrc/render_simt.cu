@@ -20,7 +20,7 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
   for (int c = 0; c < K; ++c) x[c] = 0.0f;
 #pragma unroll
   for (int pl = 0; pl < 3; ++pl) {
-    const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi);
+    const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext);
     const float gx = 1.0f - cell.fx, gy = 1.0f - cell.fy;
     const float w00 = gx * gy, w01 = cell.fx * gy, w10 = gx * cell.fy, w11 = cell.fx * cell.fy;
     const int64_t rowC = (int64_t)P.R * P.C;

@@ -26,6 +26,8 @@
 //      5. sigma/rgb are composited with an 8-lane shuffle scan per ray, the
 //         ray stops once T < term_eps, and the ray epilogue applies the DDIM
 //         update (row a6).
+//    The NG groups interleave on the SM: while one group waits on its MMA
+//    chain the others stage, scatter and run epilogues.
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -34,22 +36,21 @@
 
 namespace dmv3d {
 
-constexpr int kTcHD = 64;          // hidden width of the tensor-core engine
-constexpr int kTcKMax = 128;       // max staged texels (K) per MMA pass
-constexpr int kTcGroups = 2;       // independent 128-row groups per CTA
-constexpr int kTcThreads = 128 * kTcGroups;
-constexpr int kPatch = 4;          // 4x4 rays per patch
-constexpr int kChunk = 8;          // samples per ray per tile
+constexpr int kTcHD = 64;       // hidden width of the tensor-core engine
+constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
+constexpr int kPatch = 4;       // 4x4 rays per patch
+constexpr int kChunk = 8;       // samples per ray per tile
 constexpr uint32_t kWsHeader = 256;
 
 // shared-memory carve-up (bytes)
-constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;  // 32 KiB, K-major, SBO 2048
-constexpr uint32_t kASbo = (kTcKMax / 8) * 128;      // 2048
+constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;    // 32 KiB, K-major, SBO 2048
+constexpr uint32_t kASbo = (kTcKMax / 8) * 128;        // 2048
 constexpr uint32_t kBTileBytes = kTcKMax * kTcHD * 2;  // 16 KiB, 128 B per texel row
 constexpr uint32_t kWK = kTcHD + 16;                   // weights K incl. bias column
 constexpr uint32_t kWSbo = (kWK / 8) * 128;            // 1280
 constexpr uint32_t kWHidden = kTcHD * kWK * 2;         // 10 KiB per hidden layer
 constexpr uint32_t kWHead = 16 * kWK * 2;              // 2.5 KiB
+constexpr size_t kSmemLimit = 232448;                  // 227 KiB per CTA
 
 size_t tc_workspace_bytes(int R, int HD) { return kWsHeader + (size_t)3 * R * R * HD * 2; }
 
@@ -57,98 +58,119 @@ bool tc_supported(int K, int HD, int L) {
   return HD == kTcHD && K >= 8 && K <= 256 && K % 8 == 0 && L >= 2 && L <= kMaxLayers;
 }
 
+template <int NG>
+struct TcShared {
+  uint64_t mbar[NG];
+  uint32_t tmem_base;
+  int patch[NG];
+  int bbox[NG][2][8];  // per chunk parity: xmin,ymin,zmin,-,xmax,ymax,zmax,-
+};
+
+template <int NG>
 static size_t tc_smem_bytes(int L) {
-  return 1024 /*align slack*/ + (size_t)kTcGroups * (kATileBytes + kBTileBytes) +
-         (size_t)(L - 2) * kWHidden + kWHead + 256;
+  return 1024 /*align slack*/ + (size_t)NG * (kATileBytes + kBTileBytes) +
+         (size_t)(L - 2) * kWHidden + kWHead + sizeof(TcShared<NG>);
 }
 
 // ------------------------------------------------------------------ K0
-// G[t][o] = fp16( sum_c F[t][c] W0[o][c] + b0[o] * bscale )
+// G[t][o] = fp16(sum_c F[t][c] W0[o][c] + b0[o] * bscale); one warp per texel,
+// lane -> outputs (2 lane, 2 lane + 1); W0 transposed in smem (conflict-free).
 __global__ void __launch_bounds__(256)
     preproject_kernel(const __nv_bfloat16 *__restrict__ F, int ntex, int C,
                       const __nv_bfloat16 *__restrict__ W0, const float *__restrict__ b0,
                       float bscale, __half *__restrict__ G, unsigned int *counter) {
-  extern __shared__ __align__(16) float sw[];  // [HD][C] fp32
-  for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) sw[e] = __bfloat162float(W0[e]);
+  extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
+  for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {
+    const int o = e / C, c = e - o * C;
+    reinterpret_cast<float *>(swt)[c * kTcHD + o] = __bfloat162float(W0[e]);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0u;
   __syncthreads();
-  const int groups = kTcHD / 8;
-  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < (int64_t)ntex * groups;
-       gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = gid / groups;
-    const int og = (int)(gid - t * groups);
-    float acc[8];
-#pragma unroll
-    for (int o = 0; o < 8; ++o) acc[o] = __ldg(b0 + og * 8 + o) * bscale;
+  const int lane = threadIdx.x & 31;
+  const float bias0 = __ldg(b0 + 2 * lane) * bscale, bias1 = __ldg(b0 + 2 * lane + 1) * bscale;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntex;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float a0 = bias0, a1 = bias1;
     const uint4 *src = reinterpret_cast<const uint4 *>(F + t * C);
     for (int q = 0; q < C / 8; ++q) {
-      const uint4 u = __ldg(src + q);
+      const uint4 u = __ldg(src + q);  // same address across the warp: one broadcast request
       const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        const float2 w0 = swt[(q * 8 + 2 * e) * (kTcHD / 2) + lane];
+        const float2 w1 = swt[(q * 8 + 2 * e + 1) * (kTcHD / 2) + lane];
         const float f0 = bf16lo(uv[e]), f1 = bf16hi(uv[e]);
-        const int c = q * 8 + 2 * e;
-#pragma unroll
-        for (int o = 0; o < 8; ++o)
-          acc[o] += sw[(og * 8 + o) * C + c] * f0 + sw[(og * 8 + o) * C + c + 1] * f1;
+        a0 += w0.x * f0 + w1.x * f1;
+        a1 += w0.y * f0 + w1.y * f1;
       }
     }
-    uint32_t pk[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t lo = ptx::f32_to_f16(acc[2 * e]), hi = ptx::f32_to_f16(acc[2 * e + 1]);
-      pk[e] = lo | (hi << 16);
-    }
-    *reinterpret_cast<uint4 *>(G + t * kTcHD + og * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    const uint32_t pk = (uint32_t)ptx::f32_to_f16(a0) | ((uint32_t)ptx::f32_to_f16(a1) << 16);
+    reinterpret_cast<uint32_t *>(G + t * kTcHD)[lane] = pk;
   }
 }
 
 // ------------------------------------------------------------------ K1
-struct TcShared {
-  uint64_t mbar[kTcGroups];
-  uint32_t tmem_base;
-  int patch[kTcGroups];
-  int bbox[kTcGroups][2][8];  // per chunk parity: xmin,ymin,zmin,-,xmax,ymax,zmax,-
-};
+__device__ __forceinline__ uint32_t a_row(int m) {
+  return (uint32_t)((m >> 3) * kASbo + (m & 7) * 16);
+}
+__device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(((k >> 3) << 7) | ((k & 7) << 1)); }
 
-__device__ __forceinline__ uint32_t a_off(int m, int k) {
-  return (uint32_t)((m >> 3) * kASbo + (k >> 3) * 128 + (m & 7) * 16 + (k & 7) * 2);
+// epilogue of one MLP layer: TMEM row (HD fp32) -> ReLU -> fp16 -> A row, plus the
+// bias column (1.0 at k = HD, zeros to HD + 15)
+__device__ __forceinline__ void act_epilogue(uint32_t tmem_row, uint32_t sArow) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    ptx::tmem_ld32(tmem_row + 32 * h, v);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      const float *f = reinterpret_cast<const float *>(v) + kc * 8;
+      ptx::sts128(sArow + (uint32_t)((4 * h + kc) << 7), ptx::pack_relu_f16x2(f[0], f[1]),
+                  ptx::pack_relu_f16x2(f[2], f[3]), ptx::pack_relu_f16x2(f[4], f[5]),
+                  ptx::pack_relu_f16x2(f[6], f[7]));
+    }
+  }
+  ptx::sts128(sArow + (uint32_t)((kTcHD / 8) << 7), 0x3C00u, 0u, 0u, 0u);  // bias column = 1.0
+  ptx::sts128(sArow + (uint32_t)((kTcHD / 8 + 1) << 7), 0u, 0u, 0u, 0u);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int NG>
+__global__ void __launch_bounds__(128 * NG, 1)
     render_tc_kernel(const __grid_constant__ RenderParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   uint8_t *tileA0 = smem;
-  uint8_t *tileB0 = smem + kTcGroups * kATileBytes;
-  uint8_t *wsm = tileB0 + kTcGroups * kBTileBytes;
+  uint8_t *tileB0 = smem + NG * kATileBytes;
+  uint8_t *wsm = tileB0 + NG * kBTileBytes;
   const int L = P.L;
-  TcShared *sh = reinterpret_cast<TcShared *>(wsm + (L - 2) * kWHidden + kWHead);
+  TcShared<NG> *sh = reinterpret_cast<TcShared<NG> *>(wsm + (L - 2) * kWHidden + kWHead);
 
   const int tid_cta = threadIdx.x;
-  const int g = tid_cta >> 7;      // group
-  const int tid = tid_cta & 127;   // row within the group's tile
+  const int g = tid_cta >> 7;     // group
+  const int tid = tid_cta & 127;  // row within the group's tile
   const int warp = tid_cta >> 5;
   const int bar_id = 1 + g;
 
   // ---- prologue: barriers, TMEM, weights (fp16, K-major, bias column)
   if (tid_cta == 0) {
-    for (int i = 0; i < kTcGroups; ++i) ptx::mbar_init(&sh->mbar[i], 1);
-    for (int i = 0; i < kTcGroups; ++i)
+    for (int i = 0; i < NG; ++i) ptx::mbar_init(&sh->mbar[i], 1);
+    for (int i = 0; i < NG; ++i)
       for (int p = 0; p < 2; ++p)
         for (int e = 0; e < 8; ++e) sh->bbox[i][p][e] = (e < 4) ? 0x7fffffff : -1;
     ptx::fence_mbar_init();
   }
-  constexpr uint32_t kTmemCols = (kTcGroups * kTcHD <= 32) ? 32 : (kTcGroups * kTcHD <= 64) ? 64
-                                 : (kTcGroups * kTcHD <= 128) ? 128 : (kTcGroups * kTcHD <= 256) ? 256 : 512;
+  constexpr uint32_t kCols = NG * kTcHD;
+  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128
+                                 : kCols <= 256 ? 256 : 512;
   if (warp == 0) ptx::tmem_alloc(&sh->tmem_base, kTmemCols);
   for (int l = 1; l < L; ++l) {
     const int nout = (l == L - 1) ? 16 : kTcHD;
     const int nreal = (l == L - 1) ? 4 : kTcHD;
     uint8_t *wl = wsm + (l - 1) * kWHidden;
     const __nv_bfloat16 *W = reinterpret_cast<const __nv_bfloat16 *>(P.w[l]);
-    for (int e = tid_cta; e < nout * (int)kWK; e += kTcThreads) {
+    for (int e = tid_cta; e < nout * (int)kWK; e += 128 * NG) {
       const int n = e / kWK, k = e - n * kWK;
       float v = 0.0f;
       if (n < nreal) {
@@ -166,12 +188,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = sh->tmem_base + (uint32_t)(g * kTcHD);
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
 
-  uint8_t *tileA = tileA0 + g * kATileBytes;
-  uint8_t *tileB = tileB0 + g * kBTileBytes;
-  const uint32_t sA = ptx::smem_u32(tileA), sB = ptx::smem_u32(tileB), sW = ptx::smem_u32(wsm);
-  const uint32_t idesc_blend = ptx::idesc_f16(128, kTcHD, 1);
-  const uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
-  const uint32_t idesc_head = ptx::idesc_f16(128, 16, 0);
+  const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
+  const uint32_t sB = ptx::smem_u32(tileB0 + g * kBTileBytes);
+  const uint32_t sW = ptx::smem_u32(wsm);
+  const uint32_t sArow = sA + a_row(tid);
+  constexpr uint32_t idesc_blend = ptx::idesc_f16(128, kTcHD, 1);
+  constexpr uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
+  constexpr uint32_t idesc_head = ptx::idesc_f16(128, 16, 0);
 
   const __half *G = reinterpret_cast<const __half *>(reinterpret_cast<const uint8_t *>(P.tp) +
                                                       kWsHeader);
@@ -185,7 +208,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int64_t npatch = (int64_t)(v_hi - v_lo + 1) * PH * PW;
   const int slot = tid >> 3, q = tid & 7;
   const int R = P.R;
-  const float Rm1 = __int2float_rn(R - 1);
   const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
 
   uint32_t mphase = 0;
@@ -196,7 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (tid == 0) sh->patch[g] = (int)atomicAdd(counter, 1u);
     ptx::bar_sync(bar_id, 128);
     const int64_t patch = sh->patch[g];
-    if (patch >= npatch || P.ray_end <= P.ray_begin) break;
+    if (patch >= npatch) break;
     const int v = v_lo + (int)(patch / ((int64_t)PH * PW));
     const int prem = (int)(patch % ((int64_t)PH * PW));
     const int i = (prem / PW) * kPatch + (slot >> 2);
@@ -229,7 +251,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float p[3];
         sample_p(ray, sample_t(ray, delta, k, u), p);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) texel_coord(p[a], P.lo[a], P.hi[a], R, ix[a], fr[a]);
+        for (int a = 0; a < 3; ++a) texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, ix[a], fr[a]);
       }
       // ---- per-axis texel ranges over the tile -> per-plane bounding boxes
       {
@@ -254,70 +276,55 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         lo3[a] = sh->bbox[g][par][a];
         ext[a] = sh->bbox[g][par][4 + a] - lo3[a] + 2;  // corners: max + 1
       }
-      // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2)
-      const int bw0 = ext[0], bh0 = ext[1];
-      const int bw1 = ext[0], bh1 = ext[2];
-      const int bw2 = ext[1], bh2 = ext[2];
-      const int base1 = bw0 * bh0, base2 = base1 + bw1 * bh1;
-      const int ktot = base2 + bw2 * bh2;
       // reset the other parity's slot for the next chunk (all readers passed a barrier)
       if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
+      // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); column-major by bbox rows
+      const int bw0 = ext[0], bw1 = ext[0], bw2 = ext[1];
+      const int base1 = ext[0] * ext[1], base2 = base1 + ext[0] * ext[2];
+      const int ktot = base2 + ext[1] * ext[2];
+      const float ib0 = __frcp_rn((float)bw0), ib1 = ib0, ib2 = __frcp_rn((float)bw2);
 
-      // columns of this row's 12 corners
-      int col[3];
-      float wgt[3][4];
-      {
-        const int ca = ix[0] - lo3[0], cb = ix[1] - lo3[1], cc = ix[2] - lo3[2];
-        col[0] = cb * bw0 + ca;
-        col[1] = base1 + cc * bw1 + ca;
-        col[2] = base2 + cc * bw2 + cb;
-        const float fa[3] = {fr[0], fr[0], fr[1]}, fb[3] = {fr[1], fr[2], fr[2]};
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-          const float gx = 1.0f - fa[pl], gy = 1.0f - fb[pl];
-          wgt[pl][0] = gx * gy * wscale;
-          wgt[pl][1] = fa[pl] * gy * wscale;
-          wgt[pl][2] = gx * fb[pl] * wscale;
-          wgt[pl][3] = fa[pl] * fb[pl] * wscale;
-        }
-      }
-      const int bwp[3] = {bw0, bw1, bw2};
-      const float inv_bw0 = 1.0f / (float)bw0, inv_bw1 = 1.0f / (float)bw1,
-                  inv_bw2 = 1.0f / (float)bw2;
+      // this row's 3 plane cells -> first column of each cell
+      const int ca = ix[0] - lo3[0], cb = ix[1] - lo3[1], cc = ix[2] - lo3[2];
+      const int col0 = cb * bw0 + ca, col1 = base1 + cc * bw1 + ca, col2 = base2 + cc * bw2 + cb;
 
       // ---- blend on the tensor cores, in passes of <= kTcKMax columns
       for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
         const int kp = min(kTcKMax, ktot - w0);
         const int kpad = (kp + 15) & ~15;
         // zero this row of A, then scatter its 12 weights
-        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sA + a_off(tid, kc * 8), 0u, 0u, 0u, 0u);
+        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
         if (sv) {
+          const int cols[3] = {col0 - w0, col1 - w0, col2 - w0};
+          const int bws[3] = {bw0, bw1, bw2};
+          const float fa[3] = {fr[0], fr[0], fr[1]}, fb[3] = {fr[1], fr[2], fr[2]};
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
-            const int c0 = col[pl] - w0;
-            const int cs[4] = {c0, c0 + 1, c0 + bwp[pl], c0 + bwp[pl] + 1};
+            const float gx = 1.0f - fa[pl], gy = (1.0f - fb[pl]) * wscale, fy = fb[pl] * wscale;
+            const int c0 = cols[pl], c2 = cols[pl] + bws[pl];
+            const float w4[4] = {gx * gy, fa[pl] * gy, gx * fy, fa[pl] * fy};
+            const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (cs[e] >= 0 && cs[e] < kp) ptx::sts16(sA + a_off(tid, cs[e]), ptx::f32_to_f16(wgt[pl][e]));
+              if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
           }
         }
         // stage the texels of G for columns [w0, w0 + kpad): 8 threads per texel row
         for (int e = tid; e < kpad * 8; e += 128) {
           const int kl = e >> 3, ch = e & 7;
           const int kg = w0 + kl;
-          const uint32_t dst = sB + (uint32_t)(kl * 128 + ((ch ^ (kl & 7)) << 4));
+          const uint32_t dst = sB + (uint32_t)((kl << 7) + ((ch ^ (kl & 7)) << 4));
           if (kg < ktot) {
-            int pl, loc, bw;
-            float inv;
-            if (kg >= base2) { pl = 2; loc = kg - base2; bw = bw2; inv = inv_bw2; }
-            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = bw1; inv = inv_bw1; }
-            else { pl = 0; loc = kg; bw = bw0; inv = inv_bw0; }
-            const int rr = (int)(((float)loc + 0.5f) * inv);
-            const int cc = loc - rr * bw;
-            const int ta = (pl == 2 ? lo3[1] : lo3[0]) + cc;
-            const int tb = (pl == 0 ? lo3[1] : lo3[2]) + rr;
-            const __half *src = G + ((int64_t)(pl * R + tb) * R + ta) * kTcHD + ch * 8;
-            ptx::cp_async16(dst, src, 16u);
+            int loc, bw, ta0, tb0, pl;
+            float ib;
+            if (kg >= base2) { pl = 2; loc = kg - base2; bw = bw2; ib = ib2; ta0 = lo3[1]; tb0 = lo3[2]; }
+            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = bw1; ib = ib1; ta0 = lo3[0]; tb0 = lo3[2]; }
+            else { pl = 0; loc = kg; bw = bw0; ib = ib0; ta0 = lo3[0]; tb0 = lo3[1]; }
+            // row = floor(loc / bw): loc < 2^12, so the fp32 product is never off by one
+            const int rr = (int)(((float)loc + 0.5f) * ib);
+            const int cx = loc - rr * bw;
+            const int texel = (pl * R + tb0 + rr) * R + ta0 + cx;
+            ptx::cp_async16(dst, G + (size_t)texel * kTcHD + ch * 8, 16u);
           } else {
             ptx::cp_async16(dst, G, 0u);
           }
@@ -341,37 +348,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
       // ---- MLP layers 1..L-1 on the tensor cores (fp16 activations)
       for (int l = 1; l < L; ++l) {
-        // epilogue of the previous layer: TMEM row -> ReLU -> fp16 -> A row (+ bias column)
-        uint32_t v0[32], v1[32];
-        ptx::tmem_ld32(tmem_row, v0);
-        ptx::tmem_ld32(tmem_row + 32, v1);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int kc = 0; kc < 4; ++kc) {
-          ptx::sts128(sA + a_off(tid, kc * 8),
-                      ptx::pack_relu_f16x2(__uint_as_float(v0[kc * 8 + 0]), __uint_as_float(v0[kc * 8 + 1])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v0[kc * 8 + 2]), __uint_as_float(v0[kc * 8 + 3])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v0[kc * 8 + 4]), __uint_as_float(v0[kc * 8 + 5])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v0[kc * 8 + 6]), __uint_as_float(v0[kc * 8 + 7])));
-          ptx::sts128(sA + a_off(tid, 32 + kc * 8),
-                      ptx::pack_relu_f16x2(__uint_as_float(v1[kc * 8 + 0]), __uint_as_float(v1[kc * 8 + 1])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v1[kc * 8 + 2]), __uint_as_float(v1[kc * 8 + 3])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v1[kc * 8 + 4]), __uint_as_float(v1[kc * 8 + 5])),
-                      ptx::pack_relu_f16x2(__uint_as_float(v1[kc * 8 + 6]), __uint_as_float(v1[kc * 8 + 7])));
-        }
-        ptx::sts128(sA + a_off(tid, kTcHD), 0x3C00u, 0u, 0u, 0u);  // bias column = 1.0
-        ptx::sts128(sA + a_off(tid, kTcHD + 8), 0u, 0u, 0u, 0u);
+        act_epilogue(tmem_row, sArow);
         ptx::tc_fence_before();
         ptx::fence_proxy_async_smem();
         ptx::bar_sync(bar_id, 128);
         if (tid == 0) {
           ptx::tc_fence_after();
-          const bool head = (l == L - 1);
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
+          const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
+#pragma unroll
           for (int ks = 0; ks < (int)kWK / 16; ++ks) {
             const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
             const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ss(tmem, ad, bd, head ? idesc_head : idesc_hidden, ks > 0 ? 1u : 0u);
+            ptx::mma_f16_ss(tmem, ad, bd, id, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
         }
@@ -387,11 +376,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
         const float x = __uint_as_float(o4[0]) + P.dshift;
-        sigma = log1pf(__expf(-fabsf(x))) + fmaxf(x, 0.0f);
+        sigma = __logf(1.0f + __expf(-fabsf(x))) + fmaxf(x, 0.0f);
         const float s = 1.0f + 2.0f * P.weps;
-        c0 = s / (1.0f + __expf(-__uint_as_float(o4[1]))) - P.weps;
-        c1 = s / (1.0f + __expf(-__uint_as_float(o4[2]))) - P.weps;
-        c2 = s / (1.0f + __expf(-__uint_as_float(o4[3]))) - P.weps;
+        c0 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[1]))) - P.weps;
+        c1 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[2]))) - P.weps;
+        c2 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[3]))) - P.weps;
         n_samples++;
       }
       // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
@@ -403,7 +392,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (q >= s) S += y;
       }
       const float Tk = T * __expf(-(S - tau));
-      const float w = Tk * (-expm1f(-tau));
+      const float w = Tk * (1.0f - __expf(-tau));
       acc0 += w * c0;
       acc1 += w * c1;
       acc2 += w * c2;
@@ -448,6 +437,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // ------------------------------------------------------------------ launch
+template <int NG>
+static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
+  const size_t s1 = tc_smem_bytes<NG>(P.L);
+  cudaError_t e = cudaFuncSetAttribute(render_tc_kernel<NG>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+  if (e != cudaSuccess) return e;
+  int grid = sms;
+  if ((int64_t)grid * NG > npatch) grid = (int)((npatch + NG - 1) / NG);
+  render_tc_kernel<NG><<<grid, 128 * NG, s1, st>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   if (P0.ray_end <= P0.ray_begin) return cudaSuccess;
   if (!P0.ws) return cudaErrorInvalidValue;
@@ -461,28 +462,23 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   // K0: G = F W0^T + b0 (fp16), zero the patch counter
   const int ntex = 3 * P.R * P.R;
   const size_t s0 = (size_t)kTcHD * P.C * 4;
-  cudaError_t e = cudaFuncSetAttribute(preproject_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
+  cudaError_t e = cudaFuncSetAttribute(preproject_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
   if (e != cudaSuccess) return e;
-  const int64_t items = (int64_t)ntex * (kTcHD / 8);
-  int g0 = (int)((items + 255) / 256);
+  int g0 = (ntex * 32 + 255) / 256;
   if (g0 > sms * 8) g0 = sms * 8;
   preproject_kernel<<<g0, 256, s0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(P.tp), ntex, P.C,
                                          reinterpret_cast<const __nv_bfloat16 *>(P.w[0]), P.b[0],
                                          P.agg == 0 ? 1.0f : (1.0f / 3.0f), G, counter);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // K1: persistent render, one CTA per SM
+  // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
-  const size_t s1 = tc_smem_bytes(P.L);
-  e = cudaFuncSetAttribute(render_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-  if (e != cudaSuccess) return e;
   const int64_t HW = (int64_t)P.H * P.W;
   const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
   const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
-  int grid = sms;
-  if ((int64_t)grid * kTcGroups > npatch) grid = (int)((npatch + kTcGroups - 1) / kTcGroups);
-  render_tc_kernel<<<grid, kTcThreads, s1, st>>>(P);
-  return cudaGetLastError();
+  if (tc_smem_bytes<4>(P.L) <= kSmemLimit) return launch_k1<4>(P, sms, npatch, st);
+  return launch_k1<2>(P, sms, npatch, st);
 }
 
 }  // namespace dmv3d
