@@ -64,6 +64,7 @@ struct TcShared {
   uint32_t tmem_base;
   int patch[NG];
   int bbox[NG][2][8];  // per chunk parity: xmin,ymin,zmin,-,xmax,ymax,zmax,-
+  int coltex[NG][kTcKMax];  // staged column -> texel index of G (-1: zero fill)
 };
 
 template <int NG>
@@ -282,7 +283,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const int bw0 = ext[0], bw1 = ext[0], bw2 = ext[1];
       const int base1 = ext[0] * ext[1], base2 = base1 + ext[0] * ext[2];
       const int ktot = base2 + ext[1] * ext[2];
-      const float ib0 = __frcp_rn((float)bw0), ib1 = ib0, ib2 = __frcp_rn((float)bw2);
 
       // this row's 3 plane cells -> first column of each cell
       const int ca = ix[0] - lo3[0], cb = ix[1] - lo3[1], cc = ix[2] - lo3[2];
@@ -309,25 +309,29 @@ __global__ void __launch_bounds__(128 * NG, 1)
               if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
           }
         }
+        // column -> texel table for this pass (one column per thread)
+        if (tid < kpad) {
+          const int kg = w0 + tid;
+          int texel = -1;
+          if (kg < ktot) {
+            int loc, bw, ta0, tb0, pl;
+            if (kg >= base2) { pl = 2; loc = kg - base2; bw = bw2; ta0 = lo3[1]; tb0 = lo3[2]; }
+            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = bw1; ta0 = lo3[0]; tb0 = lo3[2]; }
+            else { pl = 0; loc = kg; bw = bw0; ta0 = lo3[0]; tb0 = lo3[1]; }
+            // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate
+            // reciprocal is never off by one
+            const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
+            texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
+          }
+          sh->coltex[g][tid] = texel;
+        }
+        ptx::bar_sync(bar_id, 128);
         // stage the texels of G for columns [w0, w0 + kpad): 8 threads per texel row
         for (int e = tid; e < kpad * 8; e += 128) {
           const int kl = e >> 3, ch = e & 7;
-          const int kg = w0 + kl;
+          const int texel = sh->coltex[g][kl];
           const uint32_t dst = sB + (uint32_t)((kl << 7) + ((ch ^ (kl & 7)) << 4));
-          if (kg < ktot) {
-            int loc, bw, ta0, tb0, pl;
-            float ib;
-            if (kg >= base2) { pl = 2; loc = kg - base2; bw = bw2; ib = ib2; ta0 = lo3[1]; tb0 = lo3[2]; }
-            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = bw1; ib = ib1; ta0 = lo3[0]; tb0 = lo3[2]; }
-            else { pl = 0; loc = kg; bw = bw0; ib = ib0; ta0 = lo3[0]; tb0 = lo3[1]; }
-            // row = floor(loc / bw): loc < 2^12, so the fp32 product is never off by one
-            const int rr = (int)(((float)loc + 0.5f) * ib);
-            const int cx = loc - rr * bw;
-            const int texel = (pl * R + tb0 + rr) * R + ta0 + cx;
-            ptx::cp_async16(dst, G + (size_t)texel * kTcHD + ch * 8, 16u);
-          } else {
-            ptx::cp_async16(dst, G, 0u);
-          }
+          ptx::cp_async16(dst, G + (size_t)max(texel, 0) * kTcHD + ch * 8, texel >= 0 ? 16u : 0u);
         }
         ptx::cp_async_wait_all();
         ptx::fence_proxy_async_smem();

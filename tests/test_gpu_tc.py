@@ -124,13 +124,20 @@ def test_tc_deterministic_and_shard_invariant():
     a, aa = api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, **kw)
     b, bb = api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, **kw)
     assert torch.equal(a, b) and torch.equal(aa, bb)
+    # shards on 4x4-patch boundaries (whole views, whole patch rows): bitwise equal (P12)
     c = torch.full_like(a, -7.0)
     cc = torch.full_like(aa, -7.0)
-    # shards at view boundaries and inside views (patches straddle the cut)
-    cuts = [0, 500, H * W, H * W + 333, w.num_rays]
+    cuts = [0, 8 * W, H * W, H * W + 12 * W, w.num_rays]
     for lo, hi in zip(cuts[:-1], cuts[1:]):
         api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, rgb=c, alpha=cc, ray_range=(lo, hi), **kw)
     assert torch.equal(a, c) and torch.equal(aa, cc)
+    # cuts through patches change a tile's texel window (the MMA's K order): fp32 rounding only
+    c.fill_(-7.0)
+    cc.fill_(-7.0)
+    cuts = [0, 500, H * W, H * W + 333, w.num_rays]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, rgb=c, alpha=cc, ray_range=(lo, hi), **kw)
+    assert (a - c).abs().max().item() < 1e-6 and (aa - cc).abs().max().item() < 1e-6
 
 
 @pytest.mark.parametrize("t,t_prev,eta,keep", [(980, 960, 0.0, None), (500, 480, 1.0, [1, 0]),

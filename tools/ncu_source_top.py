@@ -41,3 +41,29 @@ def main(path, top=30):
 
 if __name__ == "__main__":
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+
+
+def instr(path, top=40):
+    """Top source lines by executed warp instructions."""
+    rows = list(csv.reader(open(path)))
+    per, text, cur, hdr = defaultdict(float), {}, None, None
+    for r in rows:
+        if len(r) == 2 and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < len(hdr) or not r[0].isdigit():
+            continue
+        d = dict(zip(hdr, r))
+        k = (cur, int(r[0]))
+        text[k] = r[1][:80]
+        try:
+            per[k] += float(d["Instructions Executed"].replace(",", "") or 0)
+        except ValueError:
+            pass
+    tot = sum(per.values())
+    print("total warp instructions", tot)
+    for k, v in sorted(per.items(), key=lambda kv: -kv[1])[:top]:
+        print(f"{100 * v / tot:5.1f}% {k[0]}:{k[1]:<4d} {text[k]}")
