@@ -59,31 +59,42 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_ms: int = 50):
         self.gpu = gpu_index
+        self.period = period_ms
         self.rows = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._proc = None
+        self._t = threading.Thread(target=self._read, daemon=True)
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.strip().split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", f"-lms={self.period}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:  # sampler is live before timing
+                time.sleep(0.02)
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            time.sleep(2 * self.period / 1e3)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.rows:
@@ -150,7 +161,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
@@ -196,11 +207,13 @@ def main():
     rays = V * H * W
     stream = torch.cuda.current_stream(dev)
 
-    def step(i, x_in, x_out, cnt=None):
+    kernel_timer = api.Timer()
+
+    def step(i, x_in, x_out, cnt=None, timer=None):
         t, tp_ = pairs[i % len(pairs)]
         api.dmv3d_render_ddim_step(tp, intr, c2w, H, W, mlp, ab, t, tp_, x_in, None, 0.0, None,
                                    x_prev=x_out, rgb=rgb, alpha=alpha, samples_per_ray=w.samples_per_ray,
-                                   term_eps=TERM_EPS, engine=args.engine, counters=cnt)
+                                   term_eps=TERM_EPS, engine=args.engine, counters=cnt, timer=timer)
 
     # warm-up (untimed), with the kernel's own counters for evaluated samples
     for i in range(args.warmup):
@@ -222,7 +235,7 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             starts[k].record(stream)
-            step(args.warmup + k, xa, xb)
+            step(args.warmup + k, xa, xb, timer=kernel_timer)
             ends[k].record(stream)
             xa, xb = xb, xa
         barrier()
@@ -280,24 +293,29 @@ def main():
     if engine_used == "auto":
         from paper_2605_18052_b200 import _abi
         engine_used = "tcgen05" if _abi.lib() and _tc_available(api, tp, intr, c2w, H, W, mlp) else "simt"
+    k_ms, k_launches = kernel_timer.read()  # render-kernel CUDA events, timed region only
+    kernel_ms = k_ms / max(k_launches, 1)
+    launches_per_step = 2 if engine_used == "tcgen05" else 1  # (pre-projection +) render
     if engine_used == "tcgen05":
         flops = eval_samples * MLP_FLOPS_PER_SAMPLE
-        achieved = flops / (ms_per_step / 1e3) / 1e12
+        achieved = flops / (kernel_ms / 1e3) / 1e12
         peak = peaks["bf16_tflops"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": _ncu_traffic(engine_used),
                 "peak_source": f"{peak_src} dense bf16 (burst)",
+                "kernel": "render_tc_kernel", "kernel_ms": kernel_ms,
                 "algorithmic": "27,136 MLP FLOP per evaluated sample x evaluated samples per launch"}
         dtype = "bf16"
     else:
         # fp32 CUDA-core engine: MLP + gather FMAs on the FP32 pipe
         flops = eval_samples * (MLP_FLOPS_PER_SAMPLE + 2 * 12 * 80)
-        achieved = flops / (ms_per_step / 1e3) / 1e12
+        achieved = flops / (kernel_ms / 1e3) / 1e12
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # 148 SMs x 128 FP32 lanes x FMA
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": _ncu_traffic(engine_used),
                 "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
+                "kernel": "render_simt_kernel", "kernel_ms": kernel_ms,
                 "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per evaluated sample"}
         dtype = "f32"
 
@@ -327,7 +345,8 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},
-                "gpu_launches": args.steps,
+                "gpu_launches": args.steps * launches_per_step,
+                "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
                 "clocks": clk.summary(), "step_ms_min": float(step_ms.min()),
                 "step_ms_median": float(np.median(step_ms))}
         print(json.dumps(line), flush=True)

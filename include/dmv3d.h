@@ -117,7 +117,20 @@ typedef struct {
                               per-step projected triplane), ignored by SIMT.  One
                               workspace per stream: calls sharing it must be ordered. */
   uint64_t workspace_bytes;
+  struct dmv3d_timer *timer; /* optional: CUDA events are recorded around the render
+                              kernel of this call (see dmv3d_timer_*); NULL = off     */
 } dmv3d_render_opts;
+
+/* Launch timer for measurement: each render call with opts.timer set records
+ * one (start, end) CUDA-event pair on its stream around the dominant render
+ * kernel (the TCGEN05 pre-projection launch is outside the bracket).
+ * dmv3d_timer_read synchronises on the recorded events and returns the summed
+ * device time and the number of bracketed launches since the last reset. */
+typedef struct dmv3d_timer dmv3d_timer;
+dmv3d_status dmv3d_timer_create(dmv3d_timer **timer);
+dmv3d_status dmv3d_timer_destroy(dmv3d_timer *timer);
+dmv3d_status dmv3d_timer_reset(dmv3d_timer *timer);
+dmv3d_status dmv3d_timer_read(dmv3d_timer *timer, double *total_ms, int64_t *launches);
 
 /* Scratch the TCGEN05 engine needs for this triplane/MLP (0 if it cannot run
  * them): 256 + 3*R*R*hidden*2 bytes. */

@@ -22,6 +22,7 @@ EXPORTED = [
     "dmv3d_version", "dmv3d_workspace_create", "dmv3d_workspace_destroy",
     "dmv3d_render_ddim_step_host", "dmv3d_debug_ray_geometry", "dmv3d_debug_sample_points",
     "dmv3d_debug_sample_features", "dmv3d_debug_decode", "dmv3d_workspace_bytes",
+    "dmv3d_timer_create", "dmv3d_timer_destroy", "dmv3d_timer_reset", "dmv3d_timer_read",
 ]
 
 
@@ -47,7 +48,7 @@ class RenderOpts(ct.Structure):
                 ("seed", ct.c_uint64), ("bg_rgb", ct.c_float * 3), ("term_eps", ct.c_float),
                 ("ray_begin", ct.c_int64), ("ray_end", ct.c_int64), ("engine", ct.c_int32),
                 ("counters", ct.c_void_p), ("workspace", ct.c_void_p),
-                ("workspace_bytes", ct.c_uint64)]
+                ("workspace_bytes", ct.c_uint64), ("timer", ct.c_void_p)]
 
 
 class DdimParams(ct.Structure):
@@ -101,6 +102,10 @@ def lib() -> ct.CDLL:
                                                   ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_debug_decode.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int64,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
+        L.dmv3d_timer_create.argtypes = [P(ct.c_void_p)]
+        L.dmv3d_timer_destroy.argtypes = [ct.c_void_p]
+        L.dmv3d_timer_reset.argtypes = [ct.c_void_p]
+        L.dmv3d_timer_read.argtypes = [ct.c_void_p, P(ct.c_double), P(ct.c_int64)]
         L.dmv3d_workspace_bytes.argtypes = [P(Triplane), P(MLP)]
         L.dmv3d_workspace_bytes.restype = ct.c_uint64
         for name in EXPORTED:

@@ -70,13 +70,43 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
-                term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None):
+                term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None,
+                timer=None):
     b, e = (-1, -1) if ray_range is None else ray_range
     ws_ptr = None if workspace is None else workspace.data_ptr()
     ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
     return _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
                            (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
-                           None if counters is None else counters.data_ptr(), ws_ptr, ws_len)
+                           None if counters is None else counters.data_ptr(), ws_ptr, ws_len,
+                           None if timer is None else timer.handle)
+
+
+class Timer:
+    """dmv3d_timer: CUDA events the library records around each render kernel."""
+
+    def __init__(self):
+        self.handle = ct.c_void_p()
+        _abi.check(_abi.lib().dmv3d_timer_create(ct.byref(self.handle)))
+
+    def reset(self):
+        _abi.check(_abi.lib().dmv3d_timer_reset(self.handle))
+
+    def read(self):
+        """(total device ms, number of bracketed launches) since the last reset."""
+        ms, n = ct.c_double(), ct.c_int64()
+        _abi.check(_abi.lib().dmv3d_timer_read(self.handle, ct.byref(ms), ct.byref(n)))
+        return ms.value, n.value
+
+    def close(self):
+        if self.handle:
+            _abi.lib().dmv3d_timer_destroy(self.handle)
+            self.handle = ct.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _WS_CACHE = {}

@@ -15,6 +15,34 @@
 
 using namespace dmv3d;
 
+// Launch timer: a pool of CUDA event pairs recorded around each render kernel.
+struct dmv3d_timer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t used = 0;
+};
+
+namespace dmv3d {
+void timer_begin(void *t, cudaStream_t st) {
+  if (!t) return;
+  auto *tm = static_cast<dmv3d_timer *>(t);
+  if (tm->used == tm->ev.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess) return;
+    if (cudaEventCreate(&b) != cudaSuccess) {
+      cudaEventDestroy(a);
+      return;
+    }
+    tm->ev.emplace_back(a, b);
+  }
+  cudaEventRecord(tm->ev[tm->used].first, st);
+}
+void timer_end(void *t, cudaStream_t st) {
+  if (!t) return;
+  auto *tm = static_cast<dmv3d_timer *>(t);
+  if (tm->used < tm->ev.size()) cudaEventRecord(tm->ev[tm->used++].second, st);
+}
+}  // namespace dmv3d
+
 namespace {
 
 thread_local std::string g_err;
@@ -143,6 +171,7 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.counters = o->counters;
     P.ws = o->workspace;
     P.ws_bytes = o->workspace_bytes;
+    P.timer = o->timer;
   }
 }
 
@@ -269,6 +298,48 @@ extern "C" {
 
 const char *dmv3d_last_error(void) { return g_err.c_str(); }
 const char *dmv3d_version(void) { return "dmv3d-b200 0.2 (sm_100a)"; }
+
+dmv3d_status dmv3d_timer_create(dmv3d_timer **t) {
+  g_err.clear();
+  CHECK_ARG(t != nullptr, "timer is NULL");
+  *t = new dmv3d_timer();
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_timer_destroy(dmv3d_timer *t) {
+  g_err.clear();
+  if (!t) return DMV3D_OK;
+  for (auto &p : t->ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  delete t;
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_timer_reset(dmv3d_timer *t) {
+  g_err.clear();
+  CHECK_ARG(t != nullptr, "timer is NULL");
+  t->used = 0;
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_timer_read(dmv3d_timer *t, double *total_ms, int64_t *launches) {
+  g_err.clear();
+  CHECK_ARG(t && total_ms && launches, "NULL argument");
+  double tot = 0.0;
+  for (size_t i = 0; i < t->used; ++i) {
+    cudaError_t e = cudaEventSynchronize(t->ev[i].second);
+    if (e != cudaSuccess) return cuda_status(e, "timer");
+    float ms = 0.0f;
+    e = cudaEventElapsedTime(&ms, t->ev[i].first, t->ev[i].second);
+    if (e != cudaSuccess) return cuda_status(e, "timer");
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (int64_t)t->used;
+  return DMV3D_OK;
+}
 
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp) {
   if (!triplane || !mlp || triplane->res < 2) return 0;

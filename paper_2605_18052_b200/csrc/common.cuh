@@ -53,6 +53,8 @@ struct RenderParams {
   // caller-owned scratch (tensor-core engine: patch counter + projected triplane)
   void *ws;
   size_t ws_bytes;
+  // optional host-side launch timer (dmv3d_timer*): events around the render kernel
+  void *timer;
 };
 
 // ---------------------------------------------------------------- a1: rays

@@ -8,6 +8,10 @@ namespace dmv3d {
 
 constexpr int kSimtThreads = 128;
 
+// api.cu: CUDA-event bracket around the dominant (render) kernel of a call
+void timer_begin(void *timer, cudaStream_t st);
+void timer_end(void *timer, cudaStream_t st);
+
 // render_simt.cu
 bool simt_supported(int K, int HD);
 size_t simt_smem_bytes(int K, int HD, int L);

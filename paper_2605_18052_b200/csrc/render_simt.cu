@@ -338,7 +338,9 @@ cudaError_t launch_render_simt(const RenderParams &P, bool tp_bf16, bool w_bf16,
     int grid = 0;                                                                        \
     cudaError_t e = launch_cfg(fn, smem, rays, kSimtThreads, kSimtThreads / 32, st, grid); \
     if (e != cudaSuccess) return e;                                                      \
+    timer_begin(P.timer, st);                                                            \
     fn<<<grid, kSimtThreads, smem, st>>>(P, w_bf16 ? 1 : 0);                             \
+    timer_end(P.timer, st);                                                              \
     return cudaGetLastError();                                                           \
   }
   DMV3D_SIMT_SHAPES(X)

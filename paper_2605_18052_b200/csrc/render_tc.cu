@@ -481,8 +481,11 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   const int64_t HW = (int64_t)P.H * P.W;
   const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
   const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
-  if (tc_smem_bytes<4>(P.L) <= kSmemLimit) return launch_k1<4>(P, sms, npatch, st);
-  return launch_k1<2>(P, sms, npatch, st);
+  timer_begin(P.timer, st);
+  e = (tc_smem_bytes<4>(P.L) <= kSmemLimit) ? launch_k1<4>(P, sms, npatch, st)
+                                            : launch_k1<2>(P, sms, npatch, st);
+  timer_end(P.timer, st);
+  return e;
 }
 
 }  // namespace dmv3d

@@ -1,0 +1,106 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed/NCCL.
+
+The renderer shards with no data-path exchange inside a launch: rays are
+independent.  Two partitions are provided, in the priority order of §8e:
+
+* assets (`asset_shard`): a batch of assets (cfg4) is split across ranks and
+  every rank runs whole denoising loops on its own assets -- no per-step
+  communication at all (weak scaling).
+* views (`view_shard` / `denoise_step_view_sharded`): one asset's views are
+  split across ranks; per step the owner rank broadcasts the triplane S_t
+  (the reconstructor E runs on one rank), every rank renders + DDIM-updates
+  its contiguous block of views, and `all_gather_into_tensor` assembles the
+  full x_{t-1}, rgb and alpha in place on every rank.  View blocks are whole
+  4x4-patch rows, so the gathered result is bitwise equal to one GPU
+  rendering all views (pin P12).
+
+The render call is injectable (`render_fn`) so the shard/merge logic is
+tested on CPU with gloo and the CPU oracle (tests/test_dist_gloo.py); the
+default is libdmv3d's fused step.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+
+def view_shard(num_views: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of views [v0, v1) for `rank`; blocks of ceil(V/P) views,
+    the last ranks may get fewer (or none)."""
+    per = math.ceil(num_views / world)
+    v0 = min(num_views, rank * per)
+    return v0, min(num_views, v0 + per)
+
+
+def asset_shard(num_assets: int, rank: int, world: int) -> list[int]:
+    """Assets owned by `rank` (round robin)."""
+    return list(range(rank, num_assets, world))
+
+
+def _gather_views(full: torch.Tensor, v0: int, v1: int, per: int, world: int, group=None):
+    """All-gather equal blocks of `per` views into `full` [world*per, ...] in place
+    (rank r's block is full[r*per:(r+1)*per]); `full` must have world*per views."""
+    rank = dist.get_rank(group)
+    mine = full[rank * per:(rank + 1) * per]
+    try:
+        dist.all_gather_into_tensor(full, mine, group=group)
+    except (RuntimeError, NotImplementedError, ValueError):
+        # backends without all_gather_into_tensor (e.g. older gloo): list form
+        parts = list(full.split(per))  # views into `full`: gathered in place
+        dist.all_gather(parts, mine.clone(), group=group)
+
+
+def default_render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
+                      x_t, x_prev, rgb, alpha, **opts):
+    from . import api
+    if x_t is None or x_t.shape[0] == 0:
+        api.dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp, rgb=rgb, alpha=alpha,
+                               **opts)
+    else:
+        api.dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t,
+                                   t_prev, x_t, x_prev=x_prev, rgb=rgb, alpha=alpha, **opts)
+
+
+def denoise_step_view_sharded(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
+                              x_t, ddim_views: int, group=None, src: int = 0,
+                              broadcast_triplane: bool = True, render_fn=None, **opts):
+    """One denoising step of one asset, views split across the ranks of `group`.
+
+    Every rank passes full-size `intrinsics` [V,4], `c2w` [V,3,4] and `x_t`
+    [ddim_views,3,H,W] (only its own block is read).  Returns the full
+    (x_prev [ddim_views,3,H,W], rgb [V,3,H,W], alpha [V,H,W]) on every rank.
+    """
+    render_fn = render_fn or default_render_fn
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    V = int(c2w.shape[0])
+    per = math.ceil(V / world)
+    v0, v1 = view_shard(V, rank, world)
+    dev = triplane.device
+    if broadcast_triplane and world > 1:
+        dist.broadcast(triplane, src=src, group=group)
+    # full-size outputs padded to world*per views so every rank's block has the same size
+    rgb = torch.empty((world * per, 3, height, width), device=dev, dtype=torch.float32)
+    alpha = torch.empty((world * per, height, width), device=dev, dtype=torch.float32)
+    xp = torch.empty((world * per, 3, height, width), device=dev, dtype=torch.float32)
+    if v1 > v0:
+        own_dv = max(0, min(v1, ddim_views) - v0)
+        render_fn(triplane, intrinsics[v0:v1].contiguous(), c2w[v0:v1].contiguous(), height, width,
+                  mlp, alpha_bar, t, t_prev, x_t[v0:v0 + own_dv] if own_dv else None,
+                  xp[v0:v0 + own_dv] if own_dv else None, rgb[v0:v1], alpha[v0:v1], **opts)
+    if world > 1:
+        _gather_views(rgb, v0, v1, per, world, group)
+        _gather_views(alpha, v0, v1, per, world, group)
+        _gather_views(xp, v0, v1, per, world, group)
+    return xp[:ddim_views], rgb[:V], alpha[:V]
+
+
+def max_over_ranks(value: float, device, group=None) -> float:
+    """Device-timed numbers are reported as the max over ranks."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return value
+    t = torch.tensor([value], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
