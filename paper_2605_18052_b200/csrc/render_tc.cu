@@ -215,6 +215,44 @@ __global__ void __launch_bounds__(128 * NG, 1)
   unsigned long long n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;
   int chunk_ctr = 0;
 
+  // column -> texel table of the tile's window [w0, w0 + kpad) (one column per thread);
+  // `bb` = the chunk's per-axis texel ranges (min at [0..2], max at [4..6])
+  auto fill_table = [&](const int *bb, int w0) {
+    const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
+    const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
+    const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
+    const int ktot = base2 + ext1 * ext2;
+    const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
+    if (tid < kpad) {
+      const int kg = w0 + tid;
+      int texel = -1;
+      if (kg < ktot) {
+        int loc, bw, ta0, tb0, pl;
+        if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
+        else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
+        else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; }
+        // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate
+        // reciprocal is never off by one
+        const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
+        texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
+      }
+      sh->coltex[g][tid] = texel;
+    }
+  };
+  // cp.async the window's texels of G into the B tile: 8 threads per 128-B texel row,
+  // SWIZZLE_128B (16-B chunk index XOR row index within each 1 KiB atom)
+  auto stage = [&](const int *bb, int w0) {
+    const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
+    const int ktot = e0 * e1 + e0 * e2 + e1 * e2;
+    const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
+    for (int e = tid; e < kpad * 8; e += 128) {
+      const int kl = e >> 3, ch = e & 7;
+      const int texel = sh->coltex[g][kl];
+      const uint32_t dst = sB + (uint32_t)((kl << 7) + ((ch ^ (kl & 7)) << 4));
+      ptx::cp_async16(dst, G + (size_t)max(texel, 0) * kTcHD + ch * 8, texel >= 0 ? 16u : 0u);
+    }
+  };
+
   while (true) {
     if (tid == 0) sh->patch[g] = (int)atomicAdd(counter, 1u);
     ptx::bar_sync(bar_id, 128);
@@ -238,15 +276,23 @@ __global__ void __launch_bounds__(128 * NG, 1)
       n_hit += alive ? 1 : 0;
     }
 
-    for (int k0 = 0; k0 < P.N; k0 += kChunk) {
-      if (!ptx::bar_red_or(bar_id, 128, alive)) break;
-      const int par = chunk_ctr & 1;
+    // Chunk pipeline: the geometry, texel window and cp.async staging of chunk
+    // c+1 are issued while chunk c's MLP runs on the tensor cores (the staged B
+    // tile is free once c's blend MMA has completed).  Chunk c+1 is prepared for
+    // the rays alive before c's compositing; rays that terminate in c get zero A
+    // rows in c+1.
+    int ix[3] = {0, 0, 0};
+    float fr[3] = {0.f, 0.f, 0.f};
+    int par = 0;
+    // geometry + window + staging of window 0 for the chunk starting at kk (the
+    // chunk's bbox slot must still hold its reset state when this runs)
+    auto prefetch = [&](int kk, bool spec_alive) {
+      par = chunk_ctr & 1;
       ++chunk_ctr;
-      const int k = k0 + q;
-      const bool sv = alive && k < P.N;
-      // ---- a2/a3: sample point, texel cells (bit-exact fp32)
-      int ix[3] = {0, 0, 0};
-      float fr[3] = {0.f, 0.f, 0.f};
+      const int k = kk + q;
+      const bool sv = spec_alive && k < P.N;
+      ix[0] = ix[1] = ix[2] = 0;
+      fr[0] = fr[1] = fr[2] = 0.f;
       if (sv) {
         const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
         float p[3];
@@ -254,54 +300,54 @@ __global__ void __launch_bounds__(128 * NG, 1)
 #pragma unroll
         for (int a = 0; a < 3; ++a) texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, ix[a], fr[a]);
       }
-      // ---- per-axis texel ranges over the tile -> per-plane bounding boxes
-      {
-        int mn[3], mx[3];
+      int mn[3], mx[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = __reduce_min_sync(0xffffffffu, sv ? ix[a] : 0x7fffffff);
+        mx[a] = __reduce_max_sync(0xffffffffu, sv ? ix[a] : -1);
+      }
+      if ((tid & 31) == 0) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          mn[a] = __reduce_min_sync(0xffffffffu, sv ? ix[a] : 0x7fffffff);
-          mx[a] = __reduce_max_sync(0xffffffffu, sv ? ix[a] : -1);
-        }
-        if ((tid & 31) == 0) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            atomicMin(&sh->bbox[g][par][a], mn[a]);
-            atomicMax(&sh->bbox[g][par][4 + a], mx[a]);
-          }
+          atomicMin(&sh->bbox[g][par][a], mn[a]);
+          atomicMax(&sh->bbox[g][par][4 + a], mx[a]);
         }
       }
       ptx::bar_sync(bar_id, 128);
-      int lo3[3], ext[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        lo3[a] = sh->bbox[g][par][a];
-        ext[a] = sh->bbox[g][par][4 + a] - lo3[a] + 2;  // corners: max + 1
-      }
-      // reset the other parity's slot for the next chunk (all readers passed a barrier)
+      // reset the other parity's slot for the next chunk (all its readers passed a barrier)
       if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
-      // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); column-major by bbox rows
-      const int bw0 = ext[0], bw1 = ext[0], bw2 = ext[1];
-      const int base1 = ext[0] * ext[1], base2 = base1 + ext[0] * ext[2];
-      const int ktot = base2 + ext[1] * ext[2];
+      fill_table(sh->bbox[g][par], 0);
+      ptx::bar_sync(bar_id, 128);
+      stage(sh->bbox[g][par], 0);
+    };
 
-      // this row's 3 plane cells -> first column of each cell
-      const int ca = ix[0] - lo3[0], cb = ix[1] - lo3[1], cc = ix[2] - lo3[2];
-      const int col0 = cb * bw0 + ca, col1 = base1 + cc * bw1 + ca, col2 = base2 + cc * bw2 + cb;
+    bool have = ptx::bar_red_or(bar_id, 128, alive);
+    if (have) prefetch(0, alive);
+    for (int k0 = 0; have;) {
+      const int k = k0 + q;
+      const bool sv = alive && k < P.N;
+      const int *bb = sh->bbox[g][par];
+      const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
+      const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
+      // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); row-major bbox rows
+      const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
+      const int ktot = base2 + ext1 * ext2;
+      const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
+      const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
+      const int bws[3] = {ext0, ext0, ext1};
+      const float fa[3] = {fr[0], fr[0], fr[1]}, fb[3] = {fr[1], fr[2], fr[2]};
 
-      // ---- blend on the tensor cores, in passes of <= kTcKMax columns
+      // ---- blend on the tensor cores: window 0 was staged by prefetch; rare extra
+      //      windows (> kTcKMax texels) are staged synchronously
       for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
         const int kp = min(kTcKMax, ktot - w0);
         const int kpad = (kp + 15) & ~15;
-        // zero this row of A, then scatter its 12 weights
         for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
         if (sv) {
-          const int cols[3] = {col0 - w0, col1 - w0, col2 - w0};
-          const int bws[3] = {bw0, bw1, bw2};
-          const float fa[3] = {fr[0], fr[0], fr[1]}, fb[3] = {fr[1], fr[2], fr[2]};
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
             const float gx = 1.0f - fa[pl], gy = (1.0f - fb[pl]) * wscale, fy = fb[pl] * wscale;
-            const int c0 = cols[pl], c2 = cols[pl] + bws[pl];
+            const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
             const float w4[4] = {gx * gy, fa[pl] * gy, gx * fy, fa[pl] * fy};
             const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
@@ -309,29 +355,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
               if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
           }
         }
-        // column -> texel table for this pass (one column per thread)
-        if (tid < kpad) {
-          const int kg = w0 + tid;
-          int texel = -1;
-          if (kg < ktot) {
-            int loc, bw, ta0, tb0, pl;
-            if (kg >= base2) { pl = 2; loc = kg - base2; bw = bw2; ta0 = lo3[1]; tb0 = lo3[2]; }
-            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = bw1; ta0 = lo3[0]; tb0 = lo3[2]; }
-            else { pl = 0; loc = kg; bw = bw0; ta0 = lo3[0]; tb0 = lo3[1]; }
-            // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate
-            // reciprocal is never off by one
-            const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
-            texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
-          }
-          sh->coltex[g][tid] = texel;
-        }
-        ptx::bar_sync(bar_id, 128);
-        // stage the texels of G for columns [w0, w0 + kpad): 8 threads per texel row
-        for (int e = tid; e < kpad * 8; e += 128) {
-          const int kl = e >> 3, ch = e & 7;
-          const int texel = sh->coltex[g][kl];
-          const uint32_t dst = sB + (uint32_t)((kl << 7) + ((ch ^ (kl & 7)) << 4));
-          ptx::cp_async16(dst, G + (size_t)max(texel, 0) * kTcHD + ch * 8, texel >= 0 ? 16u : 0u);
+        if (w0 > 0) {  // synchronous staging of an extra window
+          fill_table(bb, w0);
+          ptx::bar_sync(bar_id, 128);
+          stage(bb, w0);
         }
         ptx::cp_async_wait_all();
         ptx::fence_proxy_async_smem();
@@ -349,6 +376,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
         mphase ^= 1u;
       }
       ptx::tc_fence_after();
+
+      // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
+      const int k1 = k0 + kChunk;
+      const bool nxt = k1 < P.N;
+      if (nxt) prefetch(k1, alive);
 
       // ---- MLP layers 1..L-1 on the tensor cores (fp16 activations)
       for (int l = 1; l < L; ++l) {
@@ -403,10 +435,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const float Stot = __shfl_sync(0xffffffffu, S, kChunk - 1, kChunk);
       T = T * __expf(-Stot);
       if (alive && P.term_eps > 0.0f && T < P.term_eps) {
-        if (k0 + kChunk < P.N && q == 0) n_term++;
+        if (nxt && q == 0) n_term++;
         alive = false;
       }
+      k0 = k1;
+      have = nxt && ptx::bar_red_or(bar_id, 128, alive);
     }
+    ptx::cp_async_wait_all();  // a prefetch for a chunk nobody needs may still be landing
     // ---- ray epilogue: reduce the 8 lanes, write rgb/alpha (+ DDIM x_{t-1})
 #pragma unroll
     for (int s = kChunk / 2; s > 0; s >>= 1) {
