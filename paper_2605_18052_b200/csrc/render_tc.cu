@@ -116,24 +116,24 @@ __device__ __forceinline__ uint32_t a_row(int m) {
 }
 __device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(((k >> 3) << 7) | ((k & 7) << 1)); }
 
-// epilogue of one MLP layer: TMEM row (HD fp32) -> ReLU -> fp16 -> A row, plus the
-// bias column (1.0 at k = HD, zeros to HD + 15)
-__device__ __forceinline__ void act_epilogue(uint32_t tmem_row, uint32_t sArow) {
+// epilogue of one MLP layer: accumulator row (HD fp32 TMEM columns at `d_row`) ->
+// ReLU -> fp16 pairs -> the next layer's A operand in TMEM at `a_row` (HD/2 columns),
+// plus the bias column (k = HD: 1.0, k = HD+1..HD+15: 0)
+__device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     uint32_t v[32];
-    ptx::tmem_ld32(tmem_row + 32 * h, v);
+    ptx::tmem_ld32(d_row + 32 * h, v);
     ptx::tmem_ld_wait();
+    uint32_t pk[16];
+    const float *f = reinterpret_cast<const float *>(v);
 #pragma unroll
-    for (int kc = 0; kc < 4; ++kc) {
-      const float *f = reinterpret_cast<const float *>(v) + kc * 8;
-      ptx::sts128(sArow + (uint32_t)((4 * h + kc) << 7), ptx::pack_relu_f16x2(f[0], f[1]),
-                  ptx::pack_relu_f16x2(f[2], f[3]), ptx::pack_relu_f16x2(f[4], f[5]),
-                  ptx::pack_relu_f16x2(f[6], f[7]));
-    }
+    for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_relu_f16x2(f[2 * e], f[2 * e + 1]);
+    ptx::tmem_st16(a_row + 16 * h, pk);
   }
-  ptx::sts128(sArow + (uint32_t)((kTcHD / 8) << 7), 0x3C00u, 0u, 0u, 0u);  // bias column = 1.0
-  ptx::sts128(sArow + (uint32_t)((kTcHD / 8 + 1) << 7), 0u, 0u, 0u, 0u);
+  const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  ptx::tmem_st8(a_row + kTcHD / 2, bias);
+  ptx::tmem_st_wait();
 }
 
 template <int NG>
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         for (int e = 0; e < 8; ++e) sh->bbox[i][p][e] = (e < 4) ? 0x7fffffff : -1;
     ptx::fence_mbar_init();
   }
-  constexpr uint32_t kCols = NG * kTcHD;
+  constexpr uint32_t kCols = NG * 2 * kTcHD;  // per group: accumulator + fp16 A operand
   constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128
                                  : kCols <= 256 ? 256 : 512;
   if (warp == 0) ptx::tmem_alloc(&sh->tmem_base, kTmemCols);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = sh->tmem_base + (uint32_t)(g * kTcHD);
+  const uint32_t tmem = sh->tmem_base + (uint32_t)(g * 2 * kTcHD);
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
 
   const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
@@ -382,11 +382,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const bool nxt = k1 < P.N;
       if (nxt) prefetch(k1, alive);
 
-      // ---- MLP layers 1..L-1 on the tensor cores (fp16 activations)
+      // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
+      //      (A operand from TMEM), weights in shared memory
       for (int l = 1; l < L; ++l) {
-        act_epilogue(tmem_row, sArow);
+        act_epilogue(tmem_row, tmem_row + kTcHD);
         ptx::tc_fence_before();
-        ptx::fence_proxy_async_smem();
         ptx::bar_sync(bar_id, 128);
         if (tid == 0) {
           ptx::tc_fence_after();
@@ -394,9 +394,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
           const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
 #pragma unroll
           for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
             const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ss(tmem, ad, bd, id, ks > 0 ? 1u : 0u);
+            ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
         }
