@@ -119,6 +119,9 @@ typedef struct {
   uint64_t workspace_bytes;
   struct dmv3d_timer *timer; /* optional: CUDA events are recorded around the render
                               kernel of this call (see dmv3d_timer_*); NULL = off     */
+  float *plucker;          /* optional DEVICE [V][6][H][W]: the Plucker ray map
+                              (o x d, d) of every rendered pixel,
+                              written during ray generation; NULL = off              */
 } dmv3d_render_opts;
 
 /* Launch timer for measurement: each render call with opts.timer set records
@@ -172,6 +175,24 @@ dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_
                                     const dmv3d_ddim_params *ddim, const float *x_t,
                                     const float *z, float *x_prev, float *rgb, float *alpha,
                                     dmv3d_stream stream);
+
+/* Plucker ray map: r = (o x d, d) per pixel, "concatenated with
+ * image pixels" as the denoiser's camera conditioning, with o,
+ * d the same bit-exact fp32 rays the renderer marches.  out [V][6][H][W]
+ * (channels m_x, m_y, m_z, d_x, d_y, d_z); opts may be NULL (all rays) or give
+ * a ray range. */
+dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_opts *opts,
+                                float *out, dmv3d_stream stream);
+
+/* Density grid: sigma (and rgb) of the shared MLP decoder at the
+ * G^3 points p_a = lo_a + (i_a/(G-1)) (hi_a - lo_a) of the triplane's box, the
+ * input of marching cubes for the paper's Chamfer-distance evaluation and mesh
+ * extraction.  sigma [G][G][G] and rgb [3][G][G][G] (NULL = not
+ * written), x fastest.  fp32 CUDA-core decode (SIMT engine shapes);
+ * 2 <= grid_res <= 2048.  `timer` may be NULL. */
+dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                dmv3d_agg agg, int32_t grid_res, float *sigma, float *rgb,
+                                struct dmv3d_timer *timer, dmv3d_stream stream);
 
 /* ------------------------------------------------------ host-buffer variant */
 /* Same step with every tensor pointer (triplane data, weights, biases,

@@ -110,6 +110,28 @@ void orc_ray_geometry(const orc_cameras *cams, const float aabb_min[3],
   }
 }
 
+/* Plucker coordinates of a pixel ray, r = (o x d, d) (LFN),  */
+/* fp32, each component two rounded products and one rounded difference. */
+void orc_plucker(const orc_cameras *cams, int64_t r, float out[6]) {
+  const float lo[3] = {-1.0f, -1.0f, -1.0f}, hi[3] = {1.0f, 1.0f, 1.0f};
+  float o[3], d[3], tn, tf;
+  int32_t hit;
+  orc_ray_geometry(cams, lo, hi, r, o, d, &tn, &tf, &hit);
+  float a, b;
+  a = o[1] * d[2];
+  b = o[2] * d[1];
+  out[0] = a - b;
+  a = o[2] * d[0];
+  b = o[0] * d[2];
+  out[1] = a - b;
+  a = o[0] * d[1];
+  b = o[1] * d[0];
+  out[2] = a - b;
+  out[3] = d[0];
+  out[4] = d[1];
+  out[5] = d[2];
+}
+
 /* Reading A10: optional stratified jitter from a portable counter-based */
 /* generator (splitmix64 finaliser).                    */
 float orc_jitter(uint64_t seed, uint64_t sample_id) {
@@ -239,6 +261,38 @@ void orc_decode_point(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg,
   out[2] = rgb[1];
   out[3] = rgb[2];
   free(h0);
+}
+
+/* Density grid for marching cubes ("CD ... marching cubes on   */
+/* the NeRF density"): G^3 points on the box, align-corners,    */
+/* p_a = lo_a + (idx_a / (G-1)) (hi_a - lo_a) in fp32; x fastest.              */
+void orc_grid_point(const float lo[3], const float hi[3], int32_t G, int64_t idx, float p[3]) {
+  const int64_t ix = idx % G, iy = (idx / G) % G, iz = idx / ((int64_t)G * G);
+  const int64_t id3[3] = {ix, iy, iz};
+  for (int a = 0; a < 3; ++a) {
+    float s = (float)id3[a] / (float)(G - 1);
+    float ext = hi[a] - lo[a];
+    float m = s * ext;
+    p[a] = lo[a] + m;
+  }
+}
+
+void orc_density_grid(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg, int32_t G,
+                      double *sigma, double *rgb, int32_t num_threads) {
+  const int64_t n = (int64_t)G * G * G;
+#ifdef _OPENMP
+  if (num_threads > 0) omp_set_num_threads(num_threads);
+#pragma omp parallel for schedule(dynamic, 64)
+#endif
+  for (int64_t q = 0; q < n; ++q) {
+    float p[3];
+    orc_grid_point(tp->aabb_min, tp->aabb_max, G, q, p);
+    double out[4];
+    orc_decode_point(tp, mlp, agg, p, out);
+    sigma[q] = out[0];
+    if (rgb)
+      for (int c = 0; c < 3; ++c) rgb[c * n + q] = out[1 + c];
+  }
 }
 
 /* ------------------------------------------------------------------ */

@@ -68,6 +68,9 @@ void orc_ray_geometry(const orc_cameras *cams, const float aabb_min[3],
                       const float aabb_max[3], int64_t r, float o[3], float d[3],
                       float *t_near, float *t_far, int32_t *hit);
 
+/* Plucker ray (o x d, d) of ray id r, fp32. */
+void orc_plucker(const orc_cameras *cams, int64_t r, float out[6]);
+
 /* portable jitter value u in [0,1) for sample id (ray*N + k) (A10). */
 float orc_jitter(uint64_t seed, uint64_t sample_id);
 
@@ -88,6 +91,12 @@ void orc_mlp_decode(const orc_mlp *mlp, const double *h0, double *sigma, double 
 /* full decode at a point: gather + MLP. out[4] = sigma, r, g, b */
 void orc_decode_point(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg,
                       const float p[3], double out[4]);
+
+/* density grid (row f3): grid point idx -> p (fp32, align-corners over the box) */
+void orc_grid_point(const float lo[3], const float hi[3], int32_t G, int64_t idx, float p[3]);
+/* sigma [G][G][G] (x fastest), rgb [3][G][G][G] or NULL; fp64 */
+void orc_density_grid(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg, int32_t G,
+                      double *sigma, double *rgb, int32_t num_threads);
 
 /* render one ray (no early termination): rgb[3], alpha. */
 void orc_render_ray(const orc_triplane *tp, const orc_cameras *cams, const orc_mlp *mlp,

@@ -169,6 +169,48 @@ def ray_geometry(cams, ray_ids, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
     return o, d, tn, tf, hit
 
 
+def plucker(cams, ray_ids):
+    """Plucker rays (o x d, d) -> [n, 6] fp32."""
+    keep = _Keep()
+    c = _cams(cams, keep)
+    L = lib()
+    L.orc_plucker.argtypes = [ct.POINTER(_Cameras), ct.c_int64, ct.POINTER(ct.c_float)]
+    out = np.zeros((len(ray_ids), 6), np.float32)
+    for q, r in enumerate(np.asarray(ray_ids, dtype=np.int64)):
+        row = np.zeros(6, np.float32)
+        L.orc_plucker(ct.byref(c), int(r), _fp(row))
+        out[q] = row
+    return out
+
+
+def grid_points(G, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    """[G^3, 3] fp32 grid points of the density grid (x fastest)."""
+    L = lib()
+    L.orc_grid_point.argtypes = [ct.POINTER(ct.c_float), ct.POINTER(ct.c_float), ct.c_int32,
+                                 ct.c_int64, ct.POINTER(ct.c_float)]
+    lo, hi = _f32(aabb_min), _f32(aabb_max)
+    out = np.zeros((G ** 3, 3), np.float32)
+    for q in range(G ** 3):
+        row = np.zeros(3, np.float32)
+        L.orc_grid_point(_fp(lo), _fp(hi), G, q, _fp(row))
+        out[q] = row
+    return out
+
+
+def density_grid(tp, m, G, agg=AGG_MEAN, threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+    """sigma [G,G,G] and rgb [3,G,G,G] (fp64) on the density grid (row f3)."""
+    keep = _Keep()
+    t = _triplane(tp, keep, aabb_min, aabb_max)
+    mm = _mlp(m, keep)
+    L = lib()
+    L.orc_density_grid.argtypes = [ct.POINTER(_Triplane), ct.POINTER(_MLP), ct.c_int32, ct.c_int32,
+                                   ct.POINTER(ct.c_double), ct.POINTER(ct.c_double), ct.c_int32]
+    sigma = np.zeros((G, G, G), np.float64)
+    rgb = np.zeros((3, G, G, G), np.float64)
+    L.orc_density_grid(ct.byref(t), ct.byref(mm), agg, G, _dp(sigma), _dp(rgb), threads)
+    return sigma, rgb
+
+
 def jitter(seed: int, sample_id: int) -> float:
     return lib().orc_jitter(seed, sample_id)
 

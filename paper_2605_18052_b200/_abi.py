@@ -23,6 +23,7 @@ EXPORTED = [
     "dmv3d_render_ddim_step_host", "dmv3d_debug_ray_geometry", "dmv3d_debug_sample_points",
     "dmv3d_debug_sample_features", "dmv3d_debug_decode", "dmv3d_workspace_bytes",
     "dmv3d_timer_create", "dmv3d_timer_destroy", "dmv3d_timer_reset", "dmv3d_timer_read",
+    "dmv3d_plucker_rays", "dmv3d_density_grid",
 ]
 
 
@@ -48,7 +49,8 @@ class RenderOpts(ct.Structure):
                 ("seed", ct.c_uint64), ("bg_rgb", ct.c_float * 3), ("term_eps", ct.c_float),
                 ("ray_begin", ct.c_int64), ("ray_end", ct.c_int64), ("engine", ct.c_int32),
                 ("counters", ct.c_void_p), ("workspace", ct.c_void_p),
-                ("workspace_bytes", ct.c_uint64), ("timer", ct.c_void_p)]
+                ("workspace_bytes", ct.c_uint64), ("timer", ct.c_void_p),
+                ("plucker", ct.c_void_p)]
 
 
 class DdimParams(ct.Structure):
@@ -101,6 +103,9 @@ def lib() -> ct.CDLL:
         L.dmv3d_debug_sample_features.argtypes = [P(Triplane), ct.c_int32, ct.c_int64,
                                                   ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_debug_decode.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int64,
+                                         ct.c_void_p, ct.c_void_p, ct.c_void_p]
+        L.dmv3d_plucker_rays.argtypes = [P(Cameras), P(RenderOpts), ct.c_void_p, ct.c_void_p]
+        L.dmv3d_density_grid.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int32, ct.c_void_p,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_timer_create.argtypes = [P(ct.c_void_p)]
         L.dmv3d_timer_destroy.argtypes = [ct.c_void_p]

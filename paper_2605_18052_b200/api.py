@@ -71,14 +71,43 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
                 term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None,
-                timer=None):
+                timer=None, plucker=None):
     b, e = (-1, -1) if ray_range is None else ray_range
     ws_ptr = None if workspace is None else workspace.data_ptr()
     ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
     return _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
                            (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
                            None if counters is None else counters.data_ptr(), ws_ptr, ws_len,
-                           None if timer is None else timer.handle)
+                           None if timer is None else timer.handle,
+                           None if plucker is None else plucker.data_ptr())
+
+
+def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg="mean",
+                       aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None):
+    """sigma [G,G,G] (+ rgb [3,G,G,G]) of the decoder on the box grid."""
+    G = int(grid_res)
+    dev = triplane.device
+    sigma = torch.empty((G, G, G), device=dev, dtype=torch.float32)
+    rgb = torch.empty((3, G, G, G), device=dev, dtype=torch.float32) if want_rgb else None
+    keep = []
+    t = triplane_struct(triplane, aabb_min, aabb_max)
+    m = mlp.struct(keep)
+    _abi.check(_abi.lib().dmv3d_density_grid(ct.byref(t), ct.byref(m), _AGG[agg], G, _ptr(sigma),
+                                             _ptr(rgb), None if timer is None else timer.handle,
+                                             _stream(dev)))
+    return sigma, rgb
+
+
+def dmv3d_plucker_rays(intrinsics, c2w, height, width, out=None, ray_range=None):
+    """Plucker ray map (o x d, d) [V,6,H,W] of the renderer's rays."""
+    V = int(c2w.shape[0])
+    if out is None:
+        out = torch.empty((V, 6, height, width), device=c2w.device, dtype=torch.float32)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    o = opts_struct(samples_per_ray=1, ray_range=ray_range)
+    _abi.check(_abi.lib().dmv3d_plucker_rays(ct.byref(c), ct.byref(o), _ptr(out),
+                                             _stream(c2w.device)))
+    return out
 
 
 class Timer:

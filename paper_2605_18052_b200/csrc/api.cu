@@ -172,6 +172,7 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.ws = o->workspace;
     P.ws_bytes = o->workspace_bytes;
     P.timer = o->timer;
+    P.plucker = o->plucker;
   }
 }
 
@@ -298,6 +299,61 @@ extern "C" {
 
 const char *dmv3d_last_error(void) { return g_err.c_str(); }
 const char *dmv3d_version(void) { return "dmv3d-b200 0.2 (sm_100a)"; }
+
+dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_opts *opts,
+                                float *out, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_cams(cams)) != DMV3D_OK) return s;
+  CHECK_ARG(out != nullptr, "plucker: out is NULL");
+  CHECK_ALIGN(out, "plucker out");
+  dmv3d_render_opts o{};
+  if (opts) {
+    o = *opts;
+  } else {
+    o.samples_per_ray = 1;
+    o.ray_begin = o.ray_end = -1;
+  }
+  if ((s = check_opts(&o, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
+    return s;
+  dmv3d_triplane t{};
+  t.res = 2;
+  t.channels = 4;
+  for (int a = 0; a < 3; ++a) {
+    t.aabb_min[a] = -1.0f;
+    t.aabb_max[a] = 1.0f;
+  }
+  RenderParams P;
+  fill_common(P, &t, cams, nullptr, &o);
+  return cuda_status(launch_plucker(P, out, reinterpret_cast<cudaStream_t>(stream)),
+                     "plucker launch");
+}
+
+dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                dmv3d_agg agg, int32_t grid_res, float *sigma, float *rgb,
+                                dmv3d_timer *timer, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
+  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
+  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  CHECK_ARG(grid_res >= 2 && grid_res <= 2048, "density grid: grid_res must be in [2, 2048]");
+  CHECK_ARG(sigma != nullptr, "density grid: sigma is NULL");
+  CHECK_ALIGN(sigma, "sigma");
+  if (rgb) CHECK_ALIGN(rgb, "rgb");
+  if (!simt_supported(mlp->in_dim, mlp->hidden))
+    return fail(DMV3D_ERR_UNSUPPORTED, "density grid: unsupported (in_dim, hidden)");
+  dmv3d_cameras c{};
+  c.num_views = c.height = c.width = 1;
+  RenderParams P;
+  fill_common(P, triplane, &c, mlp, nullptr);
+  P.agg = agg;
+  P.timer = timer;
+  return cuda_status(launch_density_grid(P, triplane->dtype == DMV3D_BF16,
+                                         mlp->dtype == DMV3D_BF16, grid_res, sigma, rgb,
+                                         reinterpret_cast<cudaStream_t>(stream)),
+                     "density grid launch");
+}
 
 dmv3d_status dmv3d_timer_create(dmv3d_timer **t) {
   g_err.clear();

@@ -55,6 +55,8 @@ struct RenderParams {
   size_t ws_bytes;
   // optional host-side launch timer (dmv3d_timer*): events around the render kernel
   void *timer;
+  // optional Plucker ray map output [V][6][H][W] (row f2), written during a1
+  float *plucker;
 };
 
 // ---------------------------------------------------------------- a1: rays
@@ -201,6 +203,20 @@ __device__ __forceinline__ float hidden_act_f(int kind, float x) {
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+// Plucker coordinates r = (o x d, d), component c in 0..5; each
+// moment component is two rounded products and one rounded difference.
+__device__ __forceinline__ float plucker_component(const Ray &ray, int c) {
+  if (c >= 3) return ray.d[c - 3];
+  const int a = (c + 1) % 3, b = (c + 2) % 3;
+  return __fsub_rn(__fmul_rn(ray.o[a], ray.d[b]), __fmul_rn(ray.o[b], ray.d[a]));
+}
+
+__device__ __forceinline__ void plucker_write(float *out, int H, int W, int v, int i, int j,
+                                              int c, const Ray &ray) {
+  const int64_t HW = (int64_t)H * W;
+  out[((int64_t)v * 6 + c) * HW + (int64_t)i * W + j] = plucker_component(ray, c);
+}
 
 // Per-ray epilogue: write rgb/alpha and, for DDIM views, x_{t-1}
 // (readings A15, A18-A20).  `ch` selects the channel this

@@ -149,6 +149,29 @@ __global__ void sample_points_kernel(const __grid_constant__ RenderParams P, flo
   }
 }
 
+// row f2: Plucker ray map [V][6][H][W] for rays [ray_begin, ray_end); one thread
+// per (ray, component) so the 6 planar stores of a warp are coalesced
+__global__ void plucker_kernel(const __grid_constant__ RenderParams P, float *out) {
+  const int64_t n = (P.ray_end - P.ray_begin) * 6;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = q % (P.ray_end - P.ray_begin);
+    const int c = (int)(q / (P.ray_end - P.ray_begin));
+    int v, i, j;
+    ray_pixel(P.ray_begin + rr, P.H, P.W, v, i, j);
+    const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    plucker_write(out, P.H, P.W, v, i, j, c, ray);
+  }
+}
+
+cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st) {
+  const int64_t n = (P.ray_end - P.ray_begin) * 6;
+  if (n <= 0) return cudaSuccess;
+  const int64_t grid = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  plucker_kernel<<<(int)grid, 256, 0, st>>>(P, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
                                 cudaStream_t st) {
   const int64_t n = P.ray_end - P.ray_begin;

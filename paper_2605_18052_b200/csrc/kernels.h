@@ -21,6 +21,8 @@ cudaError_t launch_features(const RenderParams &P, bool tp_bf16, int64_t n, cons
                             float *out, cudaStream_t st);
 cudaError_t launch_decode(const RenderParams &P, bool tp_bf16, bool w_bf16, int64_t n,
                           const float *pts, float *out, cudaStream_t st);
+cudaError_t launch_density_grid(const RenderParams &P, bool tp_bf16, bool w_bf16, int G,
+                                float *sigma, float *rgb, cudaStream_t st);
 
 // render_tc.cu (tcgen05 / TMEM engine)
 bool tc_supported(int K, int HD, int L);
@@ -35,6 +37,7 @@ struct DdimCoef {
 cudaError_t launch_ddim(const DdimCoef &c, int V, int H, int W, const float *x_t,
                         const float *x0_rgb, const float *z, const uint8_t *keep_dev,
                         float *x_prev, cudaStream_t st);
+cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st);
 cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
                                 cudaStream_t st);
 cudaError_t launch_sample_points(const RenderParams &P, float *t_k, float *points,

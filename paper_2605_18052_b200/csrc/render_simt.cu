@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kSimtThreads)
     int v, i, j;
     ray_pixel(r, P.H, P.W, v, i, j);
     const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    if (P.plucker && lane < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, lane, ray);
     n_rays++;
     if (!ray.hit) {
       if (lane < 3) ray_epilogue(P, v, i, j, lane, 0.0f, 1.0f);
@@ -287,6 +288,41 @@ __global__ void __launch_bounds__(kSimtThreads)
   }
 }
 
+// row f3: density grid for marching cubes: G^3 points on the box,
+// align-corners, x fastest; sigma [G^3] and optionally rgb [3][G^3]
+template <bool BF16, int K, int HD>
+__global__ void __launch_bounds__(kSimtThreads)
+    density_grid_kernel(const __grid_constant__ RenderParams P, int w_bf16, int G,
+                        float *__restrict__ sigma, float *__restrict__ rgb) {
+  extern __shared__ __align__(16) float smem[];
+  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  float *act = smem + mlp_smem_floats<K, HD>(P.L);
+  act = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(act) + 15) & ~uintptr_t(15));
+  __syncthreads();
+  const int64_t n = (int64_t)G * G * G;
+  const float gm1 = __int2float_rn(G - 1);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id3[3] = {q % G, (q / G) % G, q / ((int64_t)G * G)};
+    float p[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float s = __fdiv_rn(__ll2float_rn(id3[a]), gm1);
+      p[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
+    }
+    float x[K];
+    gather_features<BF16, K>(P, p, x);
+    float sg, c[3];
+    mlp_decode<K, HD>(P, m, x, act + threadIdx.x, blockDim.x, sg, c);
+    sigma[q] = sg;
+    if (rgb) {
+      rgb[q] = c[0];
+      rgb[n + q] = c[1];
+      rgb[2 * n + q] = c[2];
+    }
+  }
+}
+
 // ------------------------------------------------------------- dispatch
 size_t simt_smem_bytes(int K, int HD, int L) {
   size_t floats = (size_t)HD * K + (size_t)(L - 2) * HD * HD + 4 * HD + (size_t)(L - 1) * HD + 4;
@@ -360,6 +396,27 @@ cudaError_t launch_features(const RenderParams &P, bool tp_bf16, int64_t n, cons
     return cudaGetLastError();                                                \
   }
   X(4, 0) X(8, 0) X(16, 0) X(32, 0) X(64, 0) X(80, 0)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_density_grid(const RenderParams &P, bool tp_bf16, bool w_bf16, int G,
+                                float *sigma, float *rgb, cudaStream_t st) {
+  const int64_t n = (int64_t)G * G * G;
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = simt_smem_bytes(P.K, P.HD, P.L);
+#define X(k, h)                                                                             \
+  if (P.K == k && P.HD == h) {                                                              \
+    auto fn = tp_bf16 ? density_grid_kernel<true, k, h> : density_grid_kernel<false, k, h>; \
+    int grid = 0;                                                                           \
+    cudaError_t e = launch_cfg(fn, smem, n, kSimtThreads, kSimtThreads, st, grid);          \
+    if (e != cudaSuccess) return e;                                                         \
+    timer_begin(P.timer, st);                                                               \
+    fn<<<grid, kSimtThreads, smem, st>>>(P, w_bf16 ? 1 : 0, G, sigma, rgb);                 \
+    timer_end(P.timer, st);                                                                 \
+    return cudaGetLastError();                                                              \
+  }
+  DMV3D_SIMT_SHAPES(X)
 #undef X
   return cudaErrorInvalidValue;
 }

@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     ray.hit = false;
     ray.t_near = ray.t_far = 0.0f;
     if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
     bool alive = pix && ray.hit;
     const float delta = alive ? sample_delta(ray, P.N) : 0.0f;
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;

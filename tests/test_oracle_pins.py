@@ -394,3 +394,42 @@ def test_ddim_eta1_is_ddpm_posterior_p9(golden):
         assert abs(sig - math.sqrt((1 - abp) / (1 - abt) * b)) < 1e-10
         if t == g["t"]:
             assert abs(sig - g["sigma_t"]) < g["tol"]
+
+
+# ----------------------------------------------------------------------------- f2 Plucker rays
+def test_plucker_closed_forms():
+    """r = (o x d, d): the moment is orthogonal to d, equals p x d for any
+    point p on the ray (fp64 recompute), and vanishes for a ray through the origin."""
+    cams = wl.concat_cameras(wl.input_cameras(7, 9, 4), wl.novel_cameras(7, 9, 3, seed=8))
+    ids = np.arange(cams.num_views * 63)
+    pl = oracle.plucker(cams, ids).astype(np.float64)
+    o, d, *_ = oracle.ray_geometry(cams, ids)
+    m, dd = pl[:, :3], pl[:, 3:]
+    assert np.array_equal(dd, d.astype(np.float64))
+    assert np.max(np.abs(np.sum(m * dd, 1))) < 1e-5
+    for t in (0.7, 2.3):
+        p = o.astype(np.float64) + t * d.astype(np.float64)
+        assert np.max(np.abs(np.cross(p, d.astype(np.float64)) - m)) < 2e-6
+    ax = oracle.plucker(wl.axis_camera(15, 15), [7 * 15 + 7])[0]
+    assert np.all(ax[:3] == 0) and np.array_equal(ax[3:], np.array([-1, 0, 0], np.float32))
+
+
+# ----------------------------------------------------------------------------- f3 density grid
+def test_density_grid_on_texel_lattice():
+    """With G = R the grid points sit exactly on the texel lattice (align-corners), so
+    no interpolation happens: the density grid equals the torch MLP applied to the mean
+    of the three texels each point projects to (row f3)."""
+    R, C = 9, 8
+    tp = wl.random_triplane(R, C, seed=6)
+    m = wl.random_mlp(C, 16, 3, seed=6)
+    sigma, rgb = oracle.density_grid(tp, m, R)
+    pts = oracle.grid_points(R)
+    assert np.array_equal(pts[:R, 0], np.linspace(-1, 1, R).astype(np.float32))  # x fastest
+    assert np.all(pts[R * R * R - 1] == 1.0) and np.all(pts[0] == -1.0)
+    idx = np.stack(np.meshgrid(np.arange(R), np.arange(R), np.arange(R), indexing="ij"), -1)
+    iz, iy, ix = idx[..., 0].ravel(), idx[..., 1].ravel(), idx[..., 2].ravel()
+    t64 = tp.astype(np.float64)
+    h0 = (t64[0, iy, ix] + t64[1, iz, ix] + t64[2, iz, iy]) / 3.0
+    want = torch_mlp(m, h0)
+    assert np.max(np.abs(sigma.ravel() - want[:, 0])) < 1e-12
+    assert np.max(np.abs(rgb.reshape(3, -1).T - want[:, 1:])) < 1e-12
