@@ -191,14 +191,13 @@ void orc_point_features(const orc_triplane *tp, int32_t agg, const float p[3], d
     double w01 = fx * (1.0 - fy);
     double w10 = (1.0 - fx) * fy;
     double w11 = fx * fy;
-    const float *P = tp->data + (size_t)pl * R * R * C;
-    const float *t00 = P + ((size_t)iy * R + ix) * C;
-    const float *t01 = P + ((size_t)iy * R + ix + 1) * C;
-    const float *t10 = P + ((size_t)(iy + 1) * R + ix) * C;
-    const float *t11 = P + ((size_t)(iy + 1) * R + ix + 1) * C;
+    const double *P = tp->data + (size_t)pl * R * R * C;
+    const double *t00 = P + ((size_t)iy * R + ix) * C;
+    const double *t01 = P + ((size_t)iy * R + ix + 1) * C;
+    const double *t10 = P + ((size_t)(iy + 1) * R + ix) * C;
+    const double *t11 = P + ((size_t)(iy + 1) * R + ix + 1) * C;
     for (int32_t c = 0; c < C; ++c) {
-      double v = w00 * (double)t00[c] + w01 * (double)t01[c] + w10 * (double)t10[c] +
-                 w11 * (double)t11[c];
+      double v = w00 * t00[c] + w01 * t01[c] + w10 * t10[c] + w11 * t11[c];
       out[c] += v;
     }
   }
@@ -229,11 +228,11 @@ void orc_mlp_decode(const orc_mlp *mlp, const double *h0, double *sigma, double 
   int32_t in = mlp->in_dim;
   for (int32_t l = 0; l < L; ++l) {
     int32_t out = (l == L - 1) ? 4 : mlp->hidden;
-    const float *Wl = mlp->weights[l];
-    const float *bl = mlp->biases[l];
+    const double *Wl = mlp->weights[l];
+    const double *bl = mlp->biases[l];
     for (int32_t o = 0; o < out; ++o) {
-      double acc = (double)bl[o];
-      for (int32_t q = 0; q < in; ++q) acc += (double)Wl[(size_t)o * in + q] * cur[q];
+      double acc = bl[o];
+      for (int32_t q = 0; q < in; ++q) acc += Wl[(size_t)o * in + q] * cur[q];
       nxt[o] = (l == L - 1) ? acc : hidden_act(mlp->hidden_act, acc);
     }
     double *tmp = cur;
@@ -332,6 +331,155 @@ void orc_render_ray(const orc_triplane *tp, const orc_cameras *cams, const orc_m
   free(h0);
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = acc[ch] + T * opts->bg[ch];
   *alpha = 1.0 - T;
+}
+
+/* ------------------------------------------------------------------ */
+/* Renderer backward: "differentiable volume rendering"  */
+/* supervised by L_recon.  For one ray,  */
+/* the gradient of L = sum_ch g_ch rgb_ch + gA alpha w.r.t. the triplane */
+/* and the MLP parameters, by the chain rule through the quadrature:     */
+/*   dC/dtau_k = T_{k+1} c_k - R_k, R_k = sum_{j>k} w_j c_j + T_N bg,    */
+/*   dA/dtau_k = T_N, dC/dc_k = w_k, tau_k = sigma_k delta;              */
+/* sample positions (hence delta and the texel cells) are constants.     */
+/* Accumulates into dF [3][R][R][C], dW[l] [out][in], db[l] [out].       */
+/* ------------------------------------------------------------------ */
+static double hidden_act_grad(int32_t kind, double z) {
+  switch (kind) {
+    case ORC_ACT_SILU: {
+      double s = sigmoid(z);
+      return s + z * s * (1.0 - s);
+    }
+    case ORC_ACT_SOFTPLUS: return sigmoid(z);
+    default: return z > 0.0 ? 1.0 : 0.0;
+  }
+}
+
+void orc_render_ray_backward(const orc_triplane *tp, const orc_cameras *cams,
+                             const orc_mlp *mlp, const orc_render_opts *opts, int64_t r,
+                             const double g[3], double gA, double *dF, double *const *dW,
+                             double *const *db) {
+  float o[3], d[3], tn, tf;
+  int32_t hit;
+  orc_ray_geometry(cams, tp->aabb_min, tp->aabb_max, r, o, d, &tn, &tf, &hit);
+  if (!hit) return;
+  const int32_t N = opts->samples_per_ray, L = mlp->num_layers, K = mlp->in_dim,
+                H = mlp->hidden, R = tp->res, C = tp->channels;
+  const double delta = (double)((tf - tn) / (float)N);
+  /* per-sample storage: layer inputs h_0..h_{L-1} (h_0: K wide, others H), the
+     pre-activations z_1..z_{L-1} (H), the 4 outputs */
+  const int32_t S = K + (L - 1) * H + (L - 1) * H + 4;
+  double *buf = (double *)calloc((size_t)N * S, sizeof(double));
+  double *sig = (double *)malloc(sizeof(double) * N), *col = (double *)malloc(sizeof(double) * 3 * N);
+  float *pts = (float *)malloc(sizeof(float) * 3 * N);
+#define H_IN(k, l) (buf + (size_t)(k) * S + ((l) == 0 ? 0 : K + ((l) - 1) * H))
+#define Z_OF(k, l) (buf + (size_t)(k) * S + K + (L - 1) * H + ((l) - 1) * H) /* z_l, l>=1 */
+#define OUT(k) (buf + (size_t)(k) * S + K + 2 * (L - 1) * H)
+  for (int32_t k = 0; k < N; ++k) {
+    float tk;
+    orc_sample_point(o, d, tn, tf, N, k, opts->jitter, opts->seed, r, &tk, pts + 3 * k);
+    orc_point_features(tp, opts->agg, pts + 3 * k, H_IN(k, 0));
+    for (int32_t l = 0; l < L; ++l) {
+      const int32_t in = l == 0 ? K : H, out = l == L - 1 ? 4 : H;
+      const double *h = H_IN(k, l);
+      for (int32_t q = 0; q < out; ++q) {
+        double acc = mlp->biases[l][q];
+        for (int32_t i = 0; i < in; ++i) acc += mlp->weights[l][(size_t)q * in + i] * h[i];
+        if (l == L - 1) {
+          OUT(k)[q] = acc;
+        } else {
+          Z_OF(k, l + 1)[q] = acc;
+          H_IN(k, l + 1)[q] = hidden_act(mlp->hidden_act, acc);
+        }
+      }
+    }
+    sig[k] = softplus(OUT(k)[0] + mlp->density_shift);
+    for (int c = 0; c < 3; ++c)
+      col[3 * k + c] =
+          sigmoid(OUT(k)[1 + c]) * (1.0 + 2.0 * mlp->rgb_widen_eps) - mlp->rgb_widen_eps;
+  }
+  /* forward quadrature */
+  double *T = (double *)malloc(sizeof(double) * (N + 1)), *w = (double *)malloc(sizeof(double) * N);
+  T[0] = 1.0;
+  for (int32_t k = 0; k < N; ++k) {
+    const double tau = sig[k] * delta;
+    w[k] = T[k] * (-expm1(-tau));
+    T[k + 1] = T[k] * exp(-tau);
+  }
+  /* R_k suffix sums, then backward per sample */
+  double Rk[3];
+  for (int c = 0; c < 3; ++c) Rk[c] = T[N] * opts->bg[c];
+  double *dh = (double *)malloc(sizeof(double) * (K > H ? K : H));
+  double *delta_v = (double *)malloc(sizeof(double) * (H > 4 ? H : 4));
+  for (int32_t k = N - 1; k >= 0; --k) {
+    double dtau = gA * T[N];
+    for (int c = 0; c < 3; ++c) dtau += g[c] * (T[k + 1] * col[3 * k + c] - Rk[c]);
+    for (int c = 0; c < 3; ++c) Rk[c] += w[k] * col[3 * k + c];
+    const double s0 = sigmoid(OUT(k)[0] + mlp->density_shift);
+    delta_v[0] = dtau * delta * s0;
+    for (int c = 0; c < 3; ++c) {
+      const double s = sigmoid(OUT(k)[1 + c]);
+      delta_v[1 + c] = g[c] * w[k] * (1.0 + 2.0 * mlp->rgb_widen_eps) * s * (1.0 - s);
+    }
+    for (int32_t l = L - 1; l >= 0; --l) {
+      const int32_t in = l == 0 ? K : H, out = l == L - 1 ? 4 : H;
+      const double *h = H_IN(k, l);
+      for (int32_t q = 0; q < out; ++q) {
+        db[l][q] += delta_v[q];
+        for (int32_t i = 0; i < in; ++i) dW[l][(size_t)q * in + i] += delta_v[q] * h[i];
+      }
+      for (int32_t i = 0; i < in; ++i) {
+        double acc = 0.0;
+        for (int32_t q = 0; q < out; ++q) acc += mlp->weights[l][(size_t)q * in + i] * delta_v[q];
+        dh[i] = acc;
+      }
+      if (l > 0)
+        for (int32_t i = 0; i < in; ++i) delta_v[i] = dh[i] * hidden_act_grad(mlp->hidden_act, Z_OF(k, l)[i]);
+    }
+    /* dh = dL/dh0 -> bilinear corners of the 3 planes */
+    const double scale = opts->agg == ORC_AGG_MEAN ? 1.0 / 3.0 : 1.0;
+    for (int pl = 0; pl < 3; ++pl) {
+      const int a = PLANE_AXES[pl][0], b = PLANE_AXES[pl][1];
+      int32_t ix, iy;
+      float fxf, fyf;
+      orc_texel_coord(pts[3 * k + a], tp->aabb_min[a], tp->aabb_max[a], R, &ix, &fxf);
+      orc_texel_coord(pts[3 * k + b], tp->aabb_min[b], tp->aabb_max[b], R, &iy, &fyf);
+      const double fx = fxf, fy = fyf;
+      const double wc[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
+      const size_t off[4] = {((size_t)(pl * R + iy) * R + ix) * C, ((size_t)(pl * R + iy) * R + ix + 1) * C,
+                             ((size_t)(pl * R + iy + 1) * R + ix) * C,
+                             ((size_t)(pl * R + iy + 1) * R + ix + 1) * C};
+      for (int e = 0; e < 4; ++e)
+        for (int32_t c = 0; c < C; ++c) dF[off[e] + c] += scale * wc[e] * dh[c];
+    }
+  }
+#undef H_IN
+#undef Z_OF
+#undef OUT
+  free(buf);
+  free(sig);
+  free(col);
+  free(pts);
+  free(T);
+  free(w);
+  free(dh);
+  free(delta_v);
+}
+
+/* all views: grad_rgb [V][3][H][W], grad_alpha [V][H][W] or NULL; sequential
+   (the accumulators are shared by all rays) */
+void orc_render_backward(const orc_triplane *tp, const orc_cameras *cams, const orc_mlp *mlp,
+                         const orc_render_opts *opts, const double *grad_rgb,
+                         const double *grad_alpha, double *dF, double *const *dW,
+                         double *const *db) {
+  const int64_t HW = (int64_t)cams->height * cams->width;
+  const int64_t n = (int64_t)cams->num_views * HW;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t v = r / HW, pix = r - v * HW;
+    double g[3];
+    for (int c = 0; c < 3; ++c) g[c] = grad_rgb[(v * 3 + c) * HW + pix];
+    const double gA = grad_alpha ? grad_alpha[r] : 0.0;
+    orc_render_ray_backward(tp, cams, mlp, opts, r, g, gA, dF, dW, db);
+  }
 }
 
 void orc_render_rays(const orc_triplane *tp, const orc_cameras *cams, const orc_mlp *mlp,

@@ -37,14 +37,14 @@ extern "C" {
 
 typedef struct {
   int32_t res, channels;
-  const float *data; /* [3][res][res][channels], values exact (bf16 upcast) */
+  const double *data; /* [3][res][res][channels] (bf16/fp32 inputs upcast exactly) */
   float aabb_min[3], aabb_max[3];
 } orc_triplane;
 
 typedef struct {
   int32_t num_layers, in_dim, hidden;
-  const float *const *weights; /* L pointers, W_l [out][in] */
-  const float *const *biases;  /* L pointers, b_l [out]     */
+  const double *const *weights; /* L pointers, W_l [out][in] (inputs upcast exactly) */
+  const double *const *biases;  /* L pointers, b_l [out]     */
   int32_t hidden_act;
   double density_shift, rgb_widen_eps;
 } orc_mlp;
@@ -97,6 +97,17 @@ void orc_grid_point(const float lo[3], const float hi[3], int32_t G, int64_t idx
 /* sigma [G][G][G] (x fastest), rgb [3][G][G][G] or NULL; fp64 */
 void orc_density_grid(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg, int32_t G,
                       double *sigma, double *rgb, int32_t num_threads);
+
+/* renderer backward (row f1): dL/dS and dL/dMLP for L = <g, rgb> + <gA, alpha>,
+ * accumulated (fp64) into dF [3][R][R][C], dW[l] [out][in], db[l] [out]. */
+void orc_render_ray_backward(const orc_triplane *tp, const orc_cameras *cams,
+                             const orc_mlp *mlp, const orc_render_opts *opts, int64_t r,
+                             const double g[3], double gA, double *dF, double *const *dW,
+                             double *const *db);
+void orc_render_backward(const orc_triplane *tp, const orc_cameras *cams, const orc_mlp *mlp,
+                         const orc_render_opts *opts, const double *grad_rgb,
+                         const double *grad_alpha, double *dF, double *const *dW,
+                         double *const *db);
 
 /* render one ray (no early termination): rgb[3], alpha. */
 void orc_render_ray(const orc_triplane *tp, const orc_cameras *cams, const orc_mlp *mlp,

@@ -31,14 +31,14 @@ def build(force: bool = False) -> str:
 
 
 class _Triplane(ct.Structure):
-    _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("data", ct.POINTER(ct.c_float)),
+    _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("data", ct.POINTER(ct.c_double)),
                 ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3)]
 
 
 class _MLP(ct.Structure):
     _fields_ = [("num_layers", ct.c_int32), ("in_dim", ct.c_int32), ("hidden", ct.c_int32),
-                ("weights", ct.POINTER(ct.POINTER(ct.c_float))),
-                ("biases", ct.POINTER(ct.POINTER(ct.c_float))),
+                ("weights", ct.POINTER(ct.POINTER(ct.c_double))),
+                ("biases", ct.POINTER(ct.POINTER(ct.c_double))),
                 ("hidden_act", ct.c_int32), ("density_shift", ct.c_double),
                 ("rgb_widen_eps", ct.c_double)]
 
@@ -110,19 +110,23 @@ class _Keep:
         return a
 
 
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
 def _triplane(tp, keep, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
-    tp = keep(_f32(tp))
-    s = _Triplane(tp.shape[1], tp.shape[3], _fp(tp), (ct.c_float * 3)(*aabb_min),
+    tp = keep(_f64(tp))  # fp32 / bf16-valued inputs upcast exactly
+    s = _Triplane(tp.shape[1], tp.shape[3], _dp(tp), (ct.c_float * 3)(*aabb_min),
                   (ct.c_float * 3)(*aabb_max))
     return s
 
 
 def _mlp(m, keep):
-    ws = [keep(_f32(w)) for w in m.weights]
-    bs = [keep(_f32(b)) for b in m.biases]
+    ws = [keep(_f64(w)) for w in m.weights]
+    bs = [keep(_f64(b)) for b in m.biases]
     L = len(ws)
-    warr = keep((ct.POINTER(ct.c_float) * L)(*[_fp(w) for w in ws]))
-    barr = keep((ct.POINTER(ct.c_float) * L)(*[_fp(b) for b in bs]))
+    warr = keep((ct.POINTER(ct.c_double) * L)(*[_dp(w) for w in ws]))
+    barr = keep((ct.POINTER(ct.c_double) * L)(*[_dp(b) for b in bs]))
     hidden = ws[0].shape[0] if L > 1 else 4
     return _MLP(L, ws[0].shape[1], hidden, warr, barr, m.hidden_act, m.density_shift,
                 m.rgb_widen_eps)
@@ -181,6 +185,35 @@ def plucker(cams, ray_ids):
         L.orc_plucker(ct.byref(c), int(r), _fp(row))
         out[q] = row
     return out
+
+
+def render_backward(tp, cams, m, N, grad_rgb, grad_alpha=None, agg=AGG_MEAN, jitter=0, seed=0,
+                    bg=(1.0, 1.0, 1.0)):
+    """Gradients of L = sum(grad_rgb * rgb) + sum(grad_alpha * alpha) w.r.t. the triplane
+    and the MLP (row f1) -> (dF [3,R,R,C], [dW_l], [db_l]), fp64."""
+    keep = _Keep()
+    t = _triplane(tp, keep)
+    mm = _mlp(m, keep)
+    c = _cams(cams, keep)
+    o = _opts(N, agg, jitter, seed, bg)
+    dF = np.zeros(np.shape(tp), np.float64)
+    dW = [np.zeros(np.shape(w), np.float64) for w in m.weights]
+    db = [np.zeros(np.shape(b), np.float64) for b in m.biases]
+    L = len(dW)
+    dWp = (ct.POINTER(ct.c_double) * L)(*[_dp(x) for x in dW])
+    dbp = (ct.POINTER(ct.c_double) * L)(*[_dp(x) for x in db])
+    gr = _f64(grad_rgb)
+    ga = _f64(grad_alpha) if grad_alpha is not None else None
+    Lb = lib()
+    Lb.orc_render_backward.argtypes = [ct.POINTER(_Triplane), ct.POINTER(_Cameras),
+                                       ct.POINTER(_MLP), ct.POINTER(_Opts),
+                                       ct.POINTER(ct.c_double), ct.POINTER(ct.c_double),
+                                       ct.POINTER(ct.c_double),
+                                       ct.POINTER(ct.POINTER(ct.c_double)),
+                                       ct.POINTER(ct.POINTER(ct.c_double))]
+    Lb.orc_render_backward(ct.byref(t), ct.byref(c), ct.byref(mm), ct.byref(o), _dp(gr),
+                           _dp(ga) if ga is not None else None, _dp(dF), dWp, dbp)
+    return dF, dW, db
 
 
 def grid_points(G, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
