@@ -184,6 +184,22 @@ dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_
 dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_opts *opts,
                                 float *out, dmv3d_stream stream);
 
+/* Renderer backward: the gradient of
+ *   L = sum grad_rgb * rgb + sum grad_alpha * alpha
+ * w.r.t. the triplane and the MLP parameters, through the same rays, samples,
+ * gather, MLP and quadrature as dmv3d_render_views -- the "differentiable volume
+ * rendering" L_recon trains through.  No early termination
+ * (opts.term_eps is ignored).  grad_rgb [V][3][H][W], grad_alpha [V][H][W] or
+ * NULL; outputs are fp32 and ACCUMULATED (caller zeroes them): grad_triplane
+ * [3][R][R][C], grad_weights / grad_biases = HOST arrays of L DEVICE pointers
+ * shaped like W_l / b_l.  fp32 CUDA cores, ReLU hidden layers only; atomics make
+ * the summation order, hence the last bits, run-dependent. */
+dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                   const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
+                                   const float *grad_rgb, const float *grad_alpha,
+                                   float *grad_triplane, float *const *grad_weights,
+                                   float *const *grad_biases, dmv3d_stream stream);
+
 /* Density grid: sigma (and rgb) of the shared MLP decoder at the
  * G^3 points p_a = lo_a + (i_a/(G-1)) (hi_a - lo_a) of the triplane's box, the
  * input of marching cubes for the paper's Chamfer-distance evaluation and mesh

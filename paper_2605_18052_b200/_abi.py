@@ -23,7 +23,7 @@ EXPORTED = [
     "dmv3d_render_ddim_step_host", "dmv3d_debug_ray_geometry", "dmv3d_debug_sample_points",
     "dmv3d_debug_sample_features", "dmv3d_debug_decode", "dmv3d_workspace_bytes",
     "dmv3d_timer_create", "dmv3d_timer_destroy", "dmv3d_timer_reset", "dmv3d_timer_read",
-    "dmv3d_plucker_rays", "dmv3d_density_grid",
+    "dmv3d_plucker_rays", "dmv3d_density_grid", "dmv3d_render_backward",
 ]
 
 
@@ -105,6 +105,9 @@ def lib() -> ct.CDLL:
         L.dmv3d_debug_decode.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int64,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_plucker_rays.argtypes = [P(Cameras), P(RenderOpts), ct.c_void_p, ct.c_void_p]
+        L.dmv3d_render_backward.argtypes = [P(Triplane), P(Cameras), P(MLP), P(RenderOpts),
+                                            ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                            P(ct.c_void_p), P(ct.c_void_p), ct.c_void_p]
         L.dmv3d_density_grid.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int32, ct.c_void_p,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_timer_create.argtypes = [P(ct.c_void_p)]

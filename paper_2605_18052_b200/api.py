@@ -82,6 +82,30 @@ def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 
                            None if plucker is None else plucker.data_ptr())
 
 
+def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "DeviceMLP", grad_rgb,
+                          grad_alpha=None, aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, **opts):
+    """Gradients of <grad_rgb, rgb> + <grad_alpha, alpha> w.r.t. the triplane and the MLP
+    (row f1) -> (d_triplane [3,R,R,C] f32, [dW_l] f32, [db_l] f32)."""
+    dev = triplane.device
+    dF = torch.zeros(triplane.shape, device=dev, dtype=torch.float32)
+    dW = [torch.zeros(w.shape, device=dev, dtype=torch.float32) for w in mlp.weights]
+    db = [torch.zeros(b.shape, device=dev, dtype=torch.float32) for b in mlp.biases]
+    keep = []
+    t = triplane_struct(triplane, aabb_min, aabb_max)
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    o = opts_struct(**opts)
+    L = len(dW)
+    dWp = (ct.c_void_p * L)(*[x.data_ptr() for x in dW])
+    dbp = (ct.c_void_p * L)(*[x.data_ptr() for x in db])
+    _abi.check(_abi.lib().dmv3d_render_backward(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o),
+                                                _ptr(grad_rgb), _ptr(grad_alpha), _ptr(dF),
+                                                ct.cast(dWp, ct.POINTER(ct.c_void_p)),
+                                                ct.cast(dbp, ct.POINTER(ct.c_void_p)),
+                                                _stream(dev)))
+    return dF, dW, db
+
+
 def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg="mean",
                        aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None):
     """sigma [G,G,G] (+ rgb [3,G,G,G]) of the decoder on the box grid."""

@@ -329,6 +329,43 @@ dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_op
                      "plucker launch");
 }
 
+dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
+                                   const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
+                                   const float *grad_rgb, const float *grad_alpha,
+                                   float *grad_triplane, float *const *grad_weights,
+                                   float *const *grad_biases, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s;
+  if ((s = check_cams(cams)) != DMV3D_OK) return s;
+  if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
+  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
+  if ((s = check_opts(opts, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
+    return s;
+  CHECK_ARG(grad_rgb && grad_triplane && grad_weights && grad_biases, "backward: NULL gradient buffer");
+  CHECK_ALIGN(grad_rgb, "grad_rgb");
+  if (grad_alpha) CHECK_ALIGN(grad_alpha, "grad_alpha");
+  CHECK_ALIGN(grad_triplane, "grad_triplane");
+  if (mlp->hidden_act != DMV3D_ACT_RELU)
+    return fail(DMV3D_ERR_UNSUPPORTED, "backward: ReLU hidden layers only");
+  if (!backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers))
+    return fail(DMV3D_ERR_UNSUPPORTED, "backward: unsupported (in_dim, hidden, L)");
+  RenderParams P;
+  fill_common(P, triplane, cams, mlp, opts);
+  GradParams G{};
+  G.g_rgb = grad_rgb;
+  G.g_alpha = grad_alpha;
+  G.dF = grad_triplane;
+  for (int l = 0; l < mlp->num_layers; ++l) {
+    CHECK_ARG(grad_weights[l] && grad_biases[l], "backward: a gradient layer pointer is NULL");
+    G.dW[l] = grad_weights[l];
+    G.db[l] = grad_biases[l];
+  }
+  return cuda_status(launch_render_backward(P, G, triplane->dtype == DMV3D_BF16,
+                                            mlp->dtype == DMV3D_BF16,
+                                            reinterpret_cast<cudaStream_t>(stream)),
+                     "backward launch");
+}
+
 dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
                                 dmv3d_agg agg, int32_t grid_res, float *sigma, float *rgb,
                                 dmv3d_timer *timer, dmv3d_stream stream) {

@@ -1,0 +1,306 @@
+// backward.cu -- renderer backward: gradients of
+// L = <g_rgb, rgb> + <g_alpha, alpha> w.r.t. the triplane and the shared MLP,
+// the "differentiable volume rendering" that L_recon trains through
+// (PAPER.md:47-55, :71).  fp32 CUDA cores, ReLU hidden layers.
+//
+// One warp per ray, lane = sample in 32-sample chunks, two passes:
+//   1. forward: composite the ray to get C = sum_k w_k c_k + T_N bg and T_N;
+//   2. forward again storing every layer's input in shared memory, then per
+//      sample dC/dtau_k = T_{k+1} c_k - R_k with R_k = C - sum_{j<=k} w_j c_j
+//      (a warp prefix sum), dA/dtau_k = T_N, dC/dc_k = w_k; back through the
+//      MLP; the feature gradient is scattered to the 12 bilinear corners with
+//      fp32 atomics; weight gradients are outer products summed over the
+//      warp's 32 samples in registers (lane = output row) and added with one
+//      atomic per weight per chunk.
+// Accumulates into caller-zeroed fp32 buffers (atomic order => results are
+// deterministic only up to fp32 rounding).
+#include "common.cuh"
+#include "kernels.h"
+#include "simt_common.cuh"
+
+namespace dmv3d {
+
+constexpr int kBwThreads = 128;
+
+template <int K, int HD>
+__device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const MlpSmem &m,
+                                                  float *col, int stride, float o4[4]) {
+  // col rows: [0, K) = h0, [K + (l-1) HD, K + l HD) = h_l (l >= 1, post-ReLU)
+  const int L = P.L;
+  for (int l = 0; l < L - 1; ++l) {
+    const int in = l == 0 ? K : HD;
+    const float *hin = col + (l == 0 ? 0 : (K + (l - 1) * HD)) * stride;
+    float *hout = col + (K + l * HD) * stride;
+    for (int o = 0; o < HD; ++o) {
+      const float *wr = m.W[l] + o * in;
+      float acc = m.B[l][o];
+      for (int i = 0; i < in; i += 4) {
+        const float4 w4 = *reinterpret_cast<const float4 *>(wr + i);
+        acc += w4.x * hin[i * stride] + w4.y * hin[(i + 1) * stride] + w4.z * hin[(i + 2) * stride] +
+               w4.w * hin[(i + 3) * stride];
+      }
+      hout[o * stride] = fmaxf(acc, 0.0f);
+    }
+  }
+  const float *h = col + (L == 1 ? 0 : (K + (L - 2) * HD)) * stride;
+  const int in = L == 1 ? K : HD;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const float *wr = m.W[L - 1] + o * in;
+    float acc = m.B[L - 1][o];
+    for (int i = 0; i < in; ++i) acc += wr[i] * h[i * stride];
+    o4[o] = acc;
+  }
+}
+
+template <bool BF16, int K, int HD>
+__global__ void __launch_bounds__(kBwThreads, 1)
+    render_backward_kernel(const __grid_constant__ RenderParams P,
+                           const __grid_constant__ GradParams Gp, int w_bf16) {
+  extern __shared__ __align__(16) float smem[];
+  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  float *scratch = smem + mlp_smem_floats<K, HD>(P.L);
+  scratch = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(scratch) + 15) & ~uintptr_t(15));
+  const int L = P.L;
+  const int rows = K + (L - 1) * HD;
+  float *dstage = scratch + rows * kBwThreads;  // [warps][32 samples][HD]
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float *col = scratch + threadIdx.x;               // this lane's column (stride 128)
+  float *wcol = scratch + wib * 32;                  // the warp's 32 columns
+  float *dst = dstage + wib * 32 * HD;               // [32][HD]
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float scale = P.agg == 0 ? (1.0f / 3.0f) : 1.0f;
+  const int64_t HWp = (int64_t)P.H * P.W;
+
+  for (int64_t r = P.ray_begin + warp0; r < P.ray_end; r += nwarps) {
+    int v, i, j;
+    ray_pixel(r, P.H, P.W, v, i, j);
+    const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+    if (!ray.hit) continue;
+    const int64_t pix = (int64_t)i * P.W + j;
+    float g[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[c] = __ldg(Gp.g_rgb + ((int64_t)v * 3 + c) * HWp + pix);
+    const float gA = Gp.g_alpha ? __ldg(Gp.g_alpha + (int64_t)v * HWp + pix) : 0.0f;
+    const float delta = sample_delta(ray, P.N);
+
+    // ---- pass 1: C and T_N
+    float Tc = 1.0f, acc[3] = {0.f, 0.f, 0.f};
+    for (int k0 = 0; k0 < P.N; k0 += 32) {
+      const int k = k0 + lane;
+      const bool valid = k < P.N;
+      float sigma = 0.0f, c[3] = {0.f, 0.f, 0.f};
+      if (valid) {
+        const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
+        float p[3];
+        sample_p(ray, sample_t(ray, delta, k, u), p);
+        float x[K];
+        gather_features<BF16, K>(P, p, x);
+        mlp_decode<K, HD>(P, m, x, col, kBwThreads, sigma, c);
+      }
+      const float tau = valid ? sigma * delta : 0.0f;
+      float S = tau;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, S, s);
+        if (lane >= s) S += y;
+      }
+      const float w = Tc * expf(-(S - tau)) * (-expm1f(-tau));
+#pragma unroll
+      for (int c2 = 0; c2 < 3; ++c2) acc[c2] += w * c[c2];
+      Tc *= expf(-__shfl_sync(0xffffffffu, S, 31));
+    }
+    float Ctot[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], s);
+      Ctot[c] = acc[c] + Tc * P.bg[c];
+    }
+    const float TN = Tc;
+
+    // ---- pass 2: forward with stored activations, then backward
+    Tc = 1.0f;
+    float Pc[3] = {0.f, 0.f, 0.f};
+    for (int k0 = 0; k0 < P.N; k0 += 32) {
+      const int k = k0 + lane;
+      const bool valid = k < P.N;
+      float p[3] = {0.f, 0.f, 0.f};
+      float o4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (valid) {
+        const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
+        sample_p(ray, sample_t(ray, delta, k, u), p);
+        float x[K];
+        gather_features<BF16, K>(P, p, x);
+#pragma unroll
+        for (int c = 0; c < K; ++c) col[c * kBwThreads] = x[c];
+        mlp_forward_store<K, HD>(P, m, col, kBwThreads, o4);
+      } else {
+        for (int rr = 0; rr < rows; ++rr) col[rr * kBwThreads] = 0.0f;
+      }
+      const float z0 = o4[0] + P.dshift;
+      const float sigma = valid ? (log1pf(expf(-fabsf(z0))) + fmaxf(z0, 0.0f)) : 0.0f;
+      float c[3], sg[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        sg[q] = sigmoid_f(o4[1 + q]);
+        c[q] = valid ? sg[q] * (1.0f + 2.0f * P.weps) - P.weps : 0.0f;
+      }
+      const float tau = valid ? sigma * delta : 0.0f;
+      float S = tau;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, S, s);
+        if (lane >= s) S += y;
+      }
+      const float Tk = Tc * expf(-(S - tau));
+      const float w = Tk * (-expm1f(-tau));
+      const float Tk1 = Tk * expf(-tau);
+      float R[3], tot[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        float sc = w * c[q];
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, sc, s);
+          if (lane >= s) sc += y;
+        }
+        R[q] = Ctot[q] - (Pc[q] + sc);
+        tot[q] = __shfl_sync(0xffffffffu, sc, 31);
+      }
+      float dtau = gA * TN;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) dtau += g[q] * (Tk1 * c[q] - R[q]);
+      float d[HD];
+#pragma unroll
+      for (int q = 0; q < HD; ++q) d[q] = 0.0f;
+      if (valid) {
+        d[0] = dtau * delta * sigmoid_f(z0);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          d[1 + q] = g[q] * w * (1.0f + 2.0f * P.weps) * sg[q] * (1.0f - sg[q]);
+      }
+      // ---- back through the MLP, layer L-1 .. 0
+      for (int l = L - 1; l >= 0; --l) {
+        const int in = l == 0 ? K : HD;
+        const int out = l == L - 1 ? 4 : HD;
+        const int hrow = l == 0 ? 0 : K + (l - 1) * HD;
+        // stage this lane's delta; lanes then own output rows q for the outer product
+#pragma unroll
+        for (int q = 0; q < HD; ++q)
+          if (q < out) dst[lane * HD + q] = d[q];
+        __syncwarp();
+        for (int q = lane; q < out; q += 32) {
+          float dq[32];
+          float bsum = 0.0f;
+#pragma unroll
+          for (int s = 0; s < 32; ++s) {
+            dq[s] = dst[s * HD + q];
+            bsum += dq[s];
+          }
+          if (bsum != 0.0f) atomicAdd(Gp.db[l] + q, bsum);
+          for (int ii = 0; ii < in; ++ii) {
+            const float *hr = wcol + (hrow + ii) * kBwThreads;
+            float sum = 0.0f;
+#pragma unroll
+            for (int s = 0; s < 32; ++s) sum += dq[s] * hr[s];
+            if (sum != 0.0f) atomicAdd(Gp.dW[l] + (size_t)q * in + ii, sum);
+          }
+        }
+        __syncwarp();
+        if (l > 0) {
+          // dh = W_l^T d; ReLU mask from h_l > 0; the new delta overwrites h_l in place
+          for (int ii = 0; ii < in; ++ii) {
+            float dh = 0.0f;
+#pragma unroll
+            for (int q = 0; q < HD; ++q)
+              if (q < out) dh += m.W[l][q * in + ii] * d[q];
+            const float h = col[(hrow + ii) * kBwThreads];
+            col[(hrow + ii) * kBwThreads] = h > 0.0f ? dh : 0.0f;
+          }
+#pragma unroll
+          for (int q = 0; q < HD; ++q) d[q] = col[(hrow + q) * kBwThreads];
+        } else if (valid) {
+          // dL/dh0 -> the 12 bilinear corners of the three planes
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) {
+            const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext);
+            const float gx = 1.0f - cell.fx, gy = 1.0f - cell.fy;
+            const float wc[4] = {gx * gy * scale, cell.fx * gy * scale, gx * cell.fy * scale,
+                                 cell.fx * cell.fy * scale};
+            const int64_t rowC = (int64_t)P.R * P.C;
+            const int64_t off[4] = {cell.off, cell.off + P.C, cell.off + rowC, cell.off + rowC + P.C};
+            for (int cc = 0; cc < K; ++cc) {
+              float dh = 0.0f;
+#pragma unroll
+              for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + cc] * d[q];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (wc[e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wc[e] * dh);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      Tc *= expf(-__shfl_sync(0xffffffffu, S, 31));
+#pragma unroll
+      for (int q = 0; q < 3; ++q) Pc[q] += tot[q];
+    }
+  }
+}
+
+template <typename Fn>
+static cudaError_t bw_launch(Fn fn, size_t smem, int64_t rays, cudaStream_t st, const RenderParams &P,
+                            const GradParams &Gp, int w_bf16) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (rays + 3) / 4;
+  if (grid > sms) grid = sms;
+  timer_begin(P.timer, st);
+  fn<<<(int)grid, kBwThreads, smem, st>>>(P, Gp, w_bf16);
+  timer_end(P.timer, st);
+  return cudaGetLastError();
+}
+
+size_t backward_smem_bytes(int K, int HD, int L) {
+  const size_t mlp = (size_t)HD * K + (size_t)(L - 2) * HD * HD + 4 * HD + (size_t)(L - 1) * HD + 4;
+  return (mlp + 4 + (size_t)(K + (L - 1) * HD) * kBwThreads + (size_t)4 * 32 * HD) * 4;
+}
+
+#define DMV3D_BW_SHAPES(X) \
+  X(4, 16)                 \
+  X(8, 16)                 \
+  X(16, 32)                \
+  X(32, 64)                \
+  X(80, 64)
+
+bool backward_supported(int K, int HD, int L) {
+  if (backward_smem_bytes(K, HD, L) > 232448) return false;
+#define X(k, h) \
+  if (K == k && HD == h) return true;
+  DMV3D_BW_SHAPES(X)
+#undef X
+  return false;
+}
+
+cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, bool tp_bf16,
+                                   bool w_bf16, cudaStream_t st) {
+  const int64_t rays = P.ray_end - P.ray_begin;
+  if (rays <= 0) return cudaSuccess;
+  const size_t smem = backward_smem_bytes(P.K, P.HD, P.L);
+#define X(k, h)                                                                                  \
+  if (P.K == k && P.HD == h)                                                                     \
+    return tp_bf16 ? bw_launch(render_backward_kernel<true, k, h>, smem, rays, st, P, Gp, w_bf16) \
+                   : bw_launch(render_backward_kernel<false, k, h>, smem, rays, st, P, Gp, w_bf16);
+  DMV3D_BW_SHAPES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dmv3d

@@ -24,6 +24,18 @@ cudaError_t launch_decode(const RenderParams &P, bool tp_bf16, bool w_bf16, int6
 cudaError_t launch_density_grid(const RenderParams &P, bool tp_bf16, bool w_bf16, int G,
                                 float *sigma, float *rgb, cudaStream_t st);
 
+// backward.cu (row f1)
+struct GradParams {
+  const float *g_rgb;    // [V][3][H][W]
+  const float *g_alpha;  // [V][H][W] or null
+  float *dF;             // [3][R][R][C], fp32, accumulated
+  float *dW[kMaxLayers];  // [out][in], accumulated
+  float *db[kMaxLayers];  // [out], accumulated
+};
+bool backward_supported(int K, int HD, int L);
+cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, bool tp_bf16,
+                                   bool w_bf16, cudaStream_t st);
+
 // render_tc.cu (tcgen05 / TMEM engine)
 bool tc_supported(int K, int HD, int L);
 size_t tc_workspace_bytes(int R, int HD);
