@@ -1,0 +1,121 @@
+#!/usr/bin/env python
+"""Throughput + roofline of the SURVEY §8(f) rows beyond the headline step
+(one JSON line each; CUDA-event timing around the library's own kernel via
+dmv3d_timer, warm-up 3, L2 flushed between reps):
+
+  f1  renderer backward   rays/s  (8 views 128^2 training crops, N=128, C=80)
+  f2  Plucker ray map     rays/s  (8 views 256^2)            HBM roofline
+  f3  density grid        points/s (128^3, C=80 MLP)          FP32-pipe roofline
+
+    python tools/bench_rows.py [--reps 10]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18052_b200 import api  # noqa: E402
+from paper_2605_18052_b200 import workloads as wl  # noqa: E402
+
+FP32_PEAK = 148 * 128 * 2 * 1.965  # TFLOP/s
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {"hbm_gbs": 6650.0}
+
+
+def timed(fn, reps, flush):
+    timer = api.Timer()
+    for _ in range(3):
+        fn(None)
+    torch.cuda.synchronize()
+    timer.reset()
+    for _ in range(reps):
+        flush.zero_()
+        fn(timer)
+    torch.cuda.synchronize()
+    ms, n = timer.read()
+    return ms / max(n, 1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=10)
+    args = ap.parse_args()
+    dev = torch.device("cuda")
+    flush = torch.empty(64 << 20, device=dev)
+    pk = peaks()
+    out = []
+
+    # f2: Plucker ray map, 8 views 256^2
+    cams = wl.concat_cameras(wl.input_cameras(256, 256, 4), wl.novel_cameras(256, 256, 4))
+    intr = torch.from_numpy(cams.intrinsics).to(dev)
+    c2w = torch.from_numpy(cams.c2w).to(dev)
+    pl = torch.empty((8, 6, 256, 256), device=dev)
+
+    def f2(timer):
+        c = api.cameras_struct(intr, c2w, 256, 256)
+        o = api.opts_struct(samples_per_ray=1, timer=timer)
+        import ctypes as ct
+        api._abi.check(api._abi.lib().dmv3d_plucker_rays(ct.byref(c), ct.byref(o), pl.data_ptr(),
+                                                         api._stream(dev)))
+    ms = timed(f2, args.reps, flush)
+    rays = 8 * 256 * 256
+    gbs = rays * 24 / (ms / 1e3) / 1e9
+    out.append({"row": "f2 plucker ray map", "metric": "rays/s", "value": rays / (ms / 1e3),
+                "kernel_ms": ms, "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"],
+                                              "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                                              "algorithmic": "24 B written per ray"}})
+
+    # f3: density grid 128^3, C = 80, L = 4 (bf16 storage, fp32 SIMT decode)
+    w = wl.make_workload("cfg3")
+    tp = torch.from_numpy(w.triplane).to(dev).to(torch.bfloat16)
+    mlp = api.DeviceMLP.from_host(w.mlp, "bf16", dev)
+    G = 128
+
+    def f3(timer):
+        api.dmv3d_density_grid(tp, mlp, G, timer=timer)
+    ms = timed(f3, args.reps, flush)
+    pts = G ** 3
+    fl = pts * (27136 + 1920) / (ms / 1e3) / 1e12
+    out.append({"row": "f3 density grid", "metric": "points/s", "value": pts / (ms / 1e3),
+                "kernel_ms": ms, "config": "128^3 grid, C=80, MLP 80-64-64-64-4, bf16 storage, fp32 SIMT",
+                "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
+                             "frac": fl / FP32_PEAK,
+                             "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per point"}})
+
+    # f1: renderer backward, 8 views of 128^2 training crops, N = 128
+    cams = wl.concat_cameras(wl.input_cameras(128, 128, 4), wl.novel_cameras(128, 128, 4))
+    intr = torch.from_numpy(cams.intrinsics).to(dev)
+    c2w = torch.from_numpy(cams.c2w).to(dev)
+    g = torch.randn((8, 3, 128, 128), device=dev)
+    gA = torch.randn((8, 128, 128), device=dev)
+
+    def f1(timer):
+        api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
+                                  timer=timer)
+    ms = timed(f1, max(3, args.reps // 3), flush)
+    rays = 8 * 128 * 128
+    # algorithmic work per sample: two forward MLP+gather passes, dL/dh (MLP^T), dW (outer
+    # products) and the gather transpose
+    per = 2 * (27136 + 1920) + 27136 + 27136 + 1920
+    hitfrac = 0.95
+    fl = rays * hitfrac * 128 * per / (ms / 1e3) / 1e12
+    out.append({"row": "f1 renderer backward", "metric": "rays/s", "value": rays / (ms / 1e3),
+                "kernel_ms": ms, "config": "8 views 128^2, N=128, C=80, L=4, fp32 SIMT, atomics",
+                "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
+                             "frac": fl / FP32_PEAK,
+                             "algorithmic": f"{per} FLOP per sample x ~0.95 hit x 128 samples"}})
+    for line in out:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()
