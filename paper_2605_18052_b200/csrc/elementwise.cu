@@ -168,7 +168,9 @@ cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st) {
   const int64_t n = (P.ray_end - P.ray_begin) * 6;
   if (n <= 0) return cudaSuccess;
   const int64_t grid = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  timer_begin(P.timer, st);
   plucker_kernel<<<(int)grid, 256, 0, st>>>(P, out);
+  timer_end(P.timer, st);
   return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 from paper_2605_18052_b200 import api  # noqa: E402
 from paper_2605_18052_b200 import workloads as wl  # noqa: E402
 
-FP32_PEAK = 148 * 128 * 2 * 1.965  # TFLOP/s
+FP32_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TFLOP/s
 
 
 def peaks():
