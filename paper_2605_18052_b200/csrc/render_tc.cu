@@ -348,21 +348,12 @@ __global__ void __launch_bounds__(128 * NG, 1)
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
             const float gx = 1.0f - fa[pl], gy = (1.0f - fb[pl]) * wscale, fy = fb[pl] * wscale;
-            const int c0 = cols[pl] - w0;
-            // the cell's two texel rows: columns (c, c+1) for row y and y+1
+            const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
+            const float w4[4] = {gx * gy, fa[pl] * gy, gx * fy, fa[pl] * fy};
+            const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
-            for (int y = 0; y < 2; ++y) {
-              const int c = c0 + y * bws[pl];
-              const float wl = y ? gx * fy : gx * gy, wr = y ? fa[pl] * fy : fa[pl] * gy;
-              if (ktot <= kTcKMax && (c & 1) == 0) {
-                // both corners in one 32-bit word: one cvt, one store
-                ptx::sts32(sArow + a_col(c), ptx::pack_f16x2(wl, wr));
-              } else {
-                if ((unsigned)c < (unsigned)kp) ptx::sts16(sArow + a_col(c), ptx::f32_to_f16(wl));
-                if ((unsigned)(c + 1) < (unsigned)kp)
-                  ptx::sts16(sArow + a_col(c + 1), ptx::f32_to_f16(wr));
-              }
-            }
+            for (int e = 0; e < 4; ++e)
+              if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
           }
         }
         if (w0 > 0) {  // synchronous staging of an extra window
@@ -381,9 +372,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
             ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
-          ptx::mbar_wait(&sh->mbar[g], mphase);  // one waiter; the others sleep in bar.sync
         }
-        ptx::bar_sync(bar_id, 128);
+        ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
       }
       ptx::tc_fence_after();
@@ -409,9 +399,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
             ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
-          ptx::mbar_wait(&sh->mbar[g], mphase);  // one waiter; the others sleep in bar.sync
         }
-        ptx::bar_sync(bar_id, 128);
+        ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
         ptx::tc_fence_after();
       }
