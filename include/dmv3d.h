@@ -149,6 +149,10 @@ typedef struct {
                               x_{t-1} = x_t (image conditioning)        */
   int32_t ddim_views;      /* views [0, ddim_views) of the camera set get the update;
                               1 <= ddim_views <= min(V, 64)                          */
+  int32_t noise_in_kernel; /* eta > 0 and z == NULL: draw z in the kernel (row f4):
+                              element e of x_t gets Box-Muller of splitmix64(seed,
+                              2e+1), splitmix64(seed, 2e+2) (24-bit uniforms)        */
+  uint64_t noise_seed;
 } dmv3d_ddim_params;
 
 /* ---------------------------------------------------------------- renderer */

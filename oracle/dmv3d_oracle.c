@@ -142,6 +142,24 @@ float orc_jitter(uint64_t seed, uint64_t sample_id) {
   return (float)(z >> 40) * (1.0f / 16777216.0f);
 }
 
+/* Row f4: in-kernel DDIM noise z (fresh noise per step,     */
+/* :1102) from the same splitmix64 counter hash: element e of x_t draws   */
+/* u1 = (h(seed, 2e) >> 40 + 1) 2^-24 in (0,1], u2 = (h(seed, 2e+1) >> 40) */
+/* 2^-24 in [0,1) and z = sqrt(-2 ln u1) cos(2 pi u2) (Box-Muller), fp64.  */
+double orc_noise(uint64_t seed, uint64_t e) {
+  uint64_t z1 = seed + (2 * e + 1ull) * 0x9E3779B97F4A7C15ull;
+  z1 = (z1 ^ (z1 >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z1 = (z1 ^ (z1 >> 27)) * 0x94D049BB133111EBull;
+  z1 = z1 ^ (z1 >> 31);
+  uint64_t z2 = seed + (2 * e + 2ull) * 0x9E3779B97F4A7C15ull;
+  z2 = (z2 ^ (z2 >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z2 = (z2 ^ (z2 >> 27)) * 0x94D049BB133111EBull;
+  z2 = z2 ^ (z2 >> 31);
+  const double u1 = (double)((z1 >> 40) + 1) / 16777216.0;
+  const double u2 = (double)(z2 >> 40) / 16777216.0;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+}
+
 /* Samples: N intervals partition [t_near, t_far] (A10, A11).          */
 void orc_sample_point(const float o[3], const float d[3], float t_near, float t_far,
                       int32_t N, int32_t k, int32_t jitter, uint64_t seed, int64_t r,

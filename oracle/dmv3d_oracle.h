@@ -71,6 +71,9 @@ void orc_ray_geometry(const orc_cameras *cams, const float aabb_min[3],
 /* Plucker ray (o x d, d) of ray id r, fp32. */
 void orc_plucker(const orc_cameras *cams, int64_t r, float out[6]);
 
+/* in-kernel DDIM noise (row f4): standard normal for element e of x_t. */
+double orc_noise(uint64_t seed, uint64_t e);
+
 /* portable jitter value u in [0,1) for sample id (ray*N + k) (A10). */
 float orc_jitter(uint64_t seed, uint64_t sample_id);
 

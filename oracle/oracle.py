@@ -244,6 +244,14 @@ def density_grid(tp, m, G, agg=AGG_MEAN, threads=0, aabb_min=(-1, -1, -1), aabb_
     return sigma, rgb
 
 
+def noise(seed: int, n: int) -> np.ndarray:
+    """In-kernel DDIM noise z for elements 0..n-1 (row f4), fp64."""
+    L = lib()
+    L.orc_noise.argtypes = [ct.c_uint64, ct.c_uint64]
+    L.orc_noise.restype = ct.c_double
+    return np.array([L.orc_noise(seed, e) for e in range(n)], np.float64)
+
+
 def jitter(seed: int, sample_id: int) -> float:
     return lib().orc_jitter(seed, sample_id)
 

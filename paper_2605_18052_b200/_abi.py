@@ -57,7 +57,8 @@ class DdimParams(ct.Structure):
     _fields_ = [("alpha_bar", ct.POINTER(ct.c_double)), ("T", ct.c_int32), ("t", ct.c_int32),
                 ("t_prev", ct.c_int32), ("eta", ct.c_float), ("x0_scale", ct.c_float),
                 ("x0_shift", ct.c_float), ("keep_mask", ct.POINTER(ct.c_uint8)),
-                ("ddim_views", ct.c_int32)]
+                ("ddim_views", ct.c_int32), ("noise_in_kernel", ct.c_int32),
+                ("noise_seed", ct.c_uint64)]
 
 
 class DMV3DError(RuntimeError):

@@ -180,7 +180,7 @@ def workspace_for(triplane_s, mlp_s, device, stream=None):
 
 
 def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mask, ddim_views,
-                keep, x0_scale=2.0, x0_shift=-1.0):
+                keep, x0_scale=2.0, x0_shift=-1.0, noise_seed=None):
     ab = np.ascontiguousarray(alpha_bar, dtype=np.float64)
     keep.append(ab)
     km = None
@@ -190,7 +190,8 @@ def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mas
     return _abi.DdimParams(ab.ctypes.data_as(ct.POINTER(ct.c_double)), len(ab), t, t_prev, eta,
                            x0_scale, x0_shift,
                            km.ctypes.data_as(ct.POINTER(ct.c_uint8)) if km is not None else None,
-                           ddim_views)
+                           ddim_views, 0 if noise_seed is None else 1,
+                           0 if noise_seed is None else int(noise_seed))
 
 
 # ------------------------------------------------------------------- entry points
@@ -216,13 +217,14 @@ def dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
 
 
 def dmv3d_ddim_step(alpha_bar, t, t_prev, x_t, x0_rgb, z=None, eta=0.0, keep_mask=None,
-                    x_prev=None, x0_scale=2.0, x0_shift=-1.0):
-    """Standalone DDIM x0 -> x_{t-1} over [V,3,H,W]."""
+                    x_prev=None, x0_scale=2.0, x0_shift=-1.0, noise_seed=None):
+    """Standalone DDIM x0 -> x_{t-1} over [V,3,H,W]; z = None with
+    noise_seed set draws the fresh noise in the kernel (row f4)."""
     V, _, H, W = x_t.shape
     if x_prev is None:
         x_prev = torch.empty_like(x_t)
     keep = []
-    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, V, keep, x0_scale, x0_shift)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, V, keep, x0_scale, x0_shift, noise_seed)
     _abi.check(_abi.lib().dmv3d_ddim_step(ct.byref(d), V, H, W, _ptr(x_t), _ptr(x0_rgb), _ptr(z),
                                           _ptr(x_prev), _stream(x_t.device)))
     return x_prev
@@ -232,7 +234,7 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
                            t, t_prev, x_t, z=None, eta=0.0, keep_mask=None, x_prev=None,
                            rgb=None, alpha=None, want_rgb=True, want_alpha=True,
                            aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, x0_scale=2.0,
-                           x0_shift=-1.0, **opts):
+                           x0_shift=-1.0, noise_seed=None, **opts):
     """Fused step: render all views; views [0, x_t.shape[0]) also get x_{t-1}."""
     V = int(c2w.shape[0])
     dv = int(x_t.shape[0])
@@ -250,7 +252,7 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
     if "workspace" not in opts:
         opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(**opts)
-    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift, noise_seed)
     _abi.check(_abi.lib().dmv3d_render_ddim_step(ct.byref(tt), ct.byref(c), ct.byref(m),
                                                  ct.byref(o), ct.byref(d), _ptr(x_t), _ptr(z),
                                                  _ptr(x_prev), _ptr(rgb), _ptr(alpha),

@@ -198,6 +198,7 @@ dmv3d_status ddim_coefficients(const dmv3d_ddim_params *d, int32_t nviews, DdimC
   c.c_eps = (float)sqrt(c2);
   c.sigma_t = (float)sigma;
   c.keep_bits = 0;
+  c.noise_seed = d->noise_seed;
   if (d->keep_mask) {
     if (nviews > 64) return fail(DMV3D_ERR_UNSUPPORTED, "ddim: keep_mask supports at most 64 views");
     for (int v = 0; v < nviews; ++v)
@@ -263,7 +264,9 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
     DdimCoef k;
     if ((s = ddim_coefficients(d, d->ddim_views, k)) != DMV3D_OK) return s;
     CHECK_ARG(x_t && x_prev, "ddim: x_t / x_prev is NULL");
-    CHECK_ARG(k.sigma_t == 0.0f || z != nullptr, "ddim: eta > 0 needs z");
+    CHECK_ARG(k.sigma_t == 0.0f || z != nullptr || d->noise_in_kernel,
+              "ddim: eta > 0 needs z or noise_in_kernel");
+    P.noise_seed = k.noise_seed;
     CHECK_ALIGN(x_t, "x_t");
     CHECK_ALIGN(x_prev, "x_prev");
     if (z) CHECK_ALIGN(z, "z");
@@ -468,7 +471,8 @@ dmv3d_status dmv3d_ddim_step(const dmv3d_ddim_params *params, int32_t V, int32_t
   dmv3d_status s = ddim_coefficients(params, V, k);
   if (s != DMV3D_OK) return s;
   CHECK_ARG(x_t && x0_rgb && x_prev, "ddim_step: x_t / x0_rgb / x_prev is NULL");
-  CHECK_ARG(k.sigma_t == 0.0f || z != nullptr, "ddim_step: eta > 0 needs z");
+  CHECK_ARG(k.sigma_t == 0.0f || z != nullptr || params->noise_in_kernel,
+            "ddim_step: eta > 0 needs z or noise_in_kernel");
   CHECK_ALIGN(x_t, "x_t");
   CHECK_ALIGN(x0_rgb, "x0_rgb");
   CHECK_ALIGN(x_prev, "x_prev");

@@ -49,6 +49,7 @@ struct RenderParams {
   float *x_prev;
   float x0_scale, x0_shift;
   float sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
+  uint64_t noise_seed;  // z == null && sigma_t != 0: in-kernel noise (row f4)
   unsigned long long *counters;
   // caller-owned scratch (tensor-core engine: patch counter + projected triplane)
   void *ws;
@@ -134,6 +135,20 @@ __device__ __forceinline__ float jitter_u(uint64_t seed, uint64_t sample_id) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   z = z ^ (z >> 31);
   return __fmul_rn(__uint2float_rn((uint32_t)(z >> 40)), 1.0f / 16777216.0f);
+}
+
+// Row f4: in-kernel DDIM noise for element e of x_t, Box-Muller on two 24-bit
+// splitmix64 uniforms (u1 in (0,1], u2 in [0,1)).
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t ctr) {
+  uint64_t z = seed + ctr * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ float ddim_noise(uint64_t seed, uint64_t e) {
+  const float u1 = (float)((splitmix_at(seed, 2 * e + 1) >> 40) + 1) * (1.0f / 16777216.0f);
+  const float u2 = (float)(splitmix_at(seed, 2 * e + 2) >> 40) * (1.0f / 16777216.0f);
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
 }
 
 __device__ __forceinline__ float sample_delta(const Ray &ray, int N) {
@@ -238,7 +253,8 @@ __device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i
       const float x0 = P.x0_scale * out + P.x0_shift;
       const float eps = (xt - P.sqrt_ab_t * x0) * P.inv_sqrt_1m_ab_t;
       xp = P.sqrt_ab_p * x0 + P.c_eps * eps;
-      if (P.sigma_t != 0.0f) xp += P.sigma_t * __ldg(P.z + idx);
+      if (P.sigma_t != 0.0f)
+        xp += P.sigma_t * (P.z ? __ldg(P.z + idx) : ddim_noise(P.noise_seed, (uint64_t)idx));
     }
     P.x_prev[idx] = xp;
   }

@@ -29,7 +29,17 @@ __global__ void ddim_kernel(const __grid_constant__ DdimCoef c, int64_t per_view
       continue;
     }
     const float4 r = __ldg(x0 + q);
-    const float4 zz = (c.sigma_t != 0.0f) ? __ldg(z + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c.sigma_t != 0.0f) {
+      if (z) {
+        zz = __ldg(z + q);
+      } else {
+        zz.x = ddim_noise(c.noise_seed, 4 * q);
+        zz.y = ddim_noise(c.noise_seed, 4 * q + 1);
+        zz.z = ddim_noise(c.noise_seed, 4 * q + 2);
+        zz.w = ddim_noise(c.noise_seed, 4 * q + 3);
+      }
+    }
     float4 o;
     o.x = ddim_one(c, xt.x, r.x, zz.x);
     o.y = ddim_one(c, xt.y, r.y, zz.y);
@@ -47,8 +57,8 @@ __global__ void ddim_kernel_scalar(const __grid_constant__ DdimCoef c, int64_t p
        q += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)(q / per_view);
     const float xt = x_t[q];
-    out[q] = ((c.keep_bits >> v) & 1ull) ? xt
-                                          : ddim_one(c, xt, x0[q], c.sigma_t != 0.0f ? z[q] : 0.0f);
+    const float zq = c.sigma_t == 0.0f ? 0.0f : (z ? z[q] : ddim_noise(c.noise_seed, (uint64_t)q));
+    out[q] = ((c.keep_bits >> v) & 1ull) ? xt : ddim_one(c, xt, x0[q], zq);
   }
 }
 

@@ -45,6 +45,7 @@ cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
 struct DdimCoef {
   float x0_scale, x0_shift, sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
   uint64_t keep_bits;
+  uint64_t noise_seed;  // used when z == null and sigma_t != 0 (in-kernel noise, row f4)
 };
 cudaError_t launch_ddim(const DdimCoef &c, int V, int H, int W, const float *x_t,
                         const float *x0_rgb, const float *z, const uint8_t *keep_dev,

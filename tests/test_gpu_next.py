@@ -68,6 +68,36 @@ def test_density_grid_matches_oracle(G, dtype):
     assert s[c, c, c] > 1.0 and s[0, 0, 0] < 1.0
 
 
+def test_in_kernel_noise_ddim_matches_oracle():
+    """Row f4: eta = 1 with the noise drawn in the kernel (standalone and fused, both
+    engines) equals the oracle's DDIM step with the oracle's copy of the generator."""
+    from paper_2605_18052_b200 import schedule
+    ab = schedule.cosine_alpha_bar()
+    V, H, W = 2, 12, 12
+    x_t = wl.gaussian((V, 3, H, W), 4)
+    rgb = np.random.default_rng(3).uniform(size=(V, 3, H, W)).astype(np.float32)
+    z = oracle.noise(77, V * 3 * H * W).reshape(V, 3, H, W)
+    want = oracle.ddim_step(oracle.cosine_alpha_bar(), 500, 480, x_t, rgb, z, eta=1.0)
+    g = api.dmv3d_ddim_step(ab, 500, 480, torch.from_numpy(x_t).cuda(), torch.from_numpy(rgb).cuda(),
+                            None, 1.0, noise_seed=77).cpu().numpy()
+    assert np.max(np.abs(g - want)) < 1e-5
+    for engine, dtype in (("simt", "f32"), ("tcgen05", "bf16")):
+        tp = wl.blob_triplane(12, 32, seed=2)
+        m = wl.blob_mlp(32, 64, 4, seed=3)
+        if dtype == "bf16":
+            tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
+        cams = wl.input_cameras(H, W, V)
+        w = wl.Workload("nz", tp, cams, m, 32, dtype)
+        t, intr, c2w, mlp = dev_workload(w)
+        xp, r, a = api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, ab, 500, 480,
+                                              torch.from_numpy(x_t).cuda(), None, 1.0,
+                                              samples_per_ray=32, engine=engine, noise_seed=77)
+        orgb, _ = oracle.render_views(tp, cams, m, 32)
+        want = oracle.ddim_step(oracle.cosine_alpha_bar(), 500, 480, x_t, orgb, z, eta=1.0)
+        tol = 1e-4 if engine == "simt" else 5e-2
+        assert np.max(np.abs(xp.cpu().numpy() - want)) < tol, engine
+
+
 def _close(g, o, rel=1e-4):
     g, o = np.asarray(g, np.float64), np.asarray(o, np.float64)
     return np.max(np.abs(g - o)) <= rel * max(np.max(np.abs(o)), 1e-30) + 1e-7

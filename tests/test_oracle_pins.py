@@ -435,6 +435,19 @@ def test_density_grid_on_texel_lattice():
     assert np.max(np.abs(rgb.reshape(3, -1).T - want[:, 1:])) < 1e-12
 
 
+# ----------------------------------------------------------------------------- f4 in-kernel noise
+def test_in_kernel_noise_is_standard_normal():
+    """Row f4: the counter-based DDIM noise is N(0,1): Kolmogorov-Smirnov distance to
+    the normal CDF, moments, and no lag-1 correlation (z enters x_{t-1} = ... + sigma_t z,
+    PAPER.md:1102 'isotropic Gaussian')."""
+    from scipy import stats
+    z = oracle.noise(2024, 60000)
+    assert stats.kstest(z, "norm").statistic < 0.008
+    assert abs(z.mean()) < 0.02 and abs(z.var() - 1) < 0.03
+    assert abs(np.corrcoef(z[:-1], z[1:])[0, 1]) < 0.02
+    assert not np.array_equal(oracle.noise(1, 100), oracle.noise(2, 100))
+
+
 # ----------------------------------------------------------------------------- f1 backward
 @pytest.mark.parametrize("act,agg", [(2, oracle.AGG_MEAN), (1, oracle.AGG_SUM), (0, oracle.AGG_MEAN)])
 def test_render_backward_matches_central_differences(act, agg):
