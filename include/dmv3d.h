@@ -208,11 +208,13 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
  * G^3 points p_a = lo_a + (i_a/(G-1)) (hi_a - lo_a) of the triplane's box, the
  * input of marching cubes for the paper's Chamfer-distance evaluation and mesh
  * extraction.  sigma [G][G][G] and rgb [3][G][G][G] (NULL = not
- * written), x fastest.  fp32 CUDA-core decode (SIMT engine shapes);
- * 2 <= grid_res <= 2048.  `timer` may be NULL. */
+ * written), x fastest; 2 <= grid_res <= 2048.  From `opts` (NULL = SIMT, mean)
+ * only agg, engine, workspace and timer are read: the TCGEN05 engine decodes
+ * 8x4x4 blocks of points through the same staged-texel blend + MLP MMAs as the
+ * renderer (needs the workspace), SIMT in fp32. */
 dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
-                                dmv3d_agg agg, int32_t grid_res, float *sigma, float *rgb,
-                                struct dmv3d_timer *timer, dmv3d_stream stream);
+                                const dmv3d_render_opts *opts, int32_t grid_res, float *sigma,
+                                float *rgb, dmv3d_stream stream);
 
 /* ------------------------------------------------------ host-buffer variant */
 /* Same step with every tensor pointer (triplane data, weights, biases,

@@ -109,7 +109,7 @@ def lib() -> ct.CDLL:
         L.dmv3d_render_backward.argtypes = [P(Triplane), P(Cameras), P(MLP), P(RenderOpts),
                                             ct.c_void_p, ct.c_void_p, ct.c_void_p,
                                             P(ct.c_void_p), P(ct.c_void_p), ct.c_void_p]
-        L.dmv3d_density_grid.argtypes = [P(Triplane), P(MLP), ct.c_int32, ct.c_int32, ct.c_void_p,
+        L.dmv3d_density_grid.argtypes = [P(Triplane), P(MLP), P(RenderOpts), ct.c_int32,
                                          ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_timer_create.argtypes = [P(ct.c_void_p)]
         L.dmv3d_timer_destroy.argtypes = [ct.c_void_p]

@@ -107,7 +107,7 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
 
 
 def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg="mean",
-                       aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None):
+                       aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None, engine="auto"):
     """sigma [G,G,G] (+ rgb [3,G,G,G]) of the decoder on the box grid."""
     G = int(grid_res)
     dev = triplane.device
@@ -116,9 +116,10 @@ def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg=
     keep = []
     t = triplane_struct(triplane, aabb_min, aabb_max)
     m = mlp.struct(keep)
-    _abi.check(_abi.lib().dmv3d_density_grid(ct.byref(t), ct.byref(m), _AGG[agg], G, _ptr(sigma),
-                                             _ptr(rgb), None if timer is None else timer.handle,
-                                             _stream(dev)))
+    ws = workspace_for(t, m, dev, torch.cuda.current_stream(dev))
+    o = opts_struct(agg=agg, engine=engine, workspace=ws, timer=timer)
+    _abi.check(_abi.lib().dmv3d_density_grid(ct.byref(t), ct.byref(m), ct.byref(o), G, _ptr(sigma),
+                                             _ptr(rgb), _stream(dev)))
     return sigma, rgb
 
 

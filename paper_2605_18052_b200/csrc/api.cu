@@ -370,25 +370,46 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
 }
 
 dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
-                                dmv3d_agg agg, int32_t grid_res, float *sigma, float *rgb,
-                                dmv3d_timer *timer, dmv3d_stream stream) {
+                                const dmv3d_render_opts *opts, int32_t grid_res, float *sigma,
+                                float *rgb, dmv3d_stream stream) {
   g_err.clear();
   dmv3d_status s;
   if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
   if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
-  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  dmv3d_render_opts o{};
+  o.samples_per_ray = 1;
+  o.ray_begin = o.ray_end = -1;
+  o.engine = DMV3D_ENGINE_SIMT;
+  if (opts) {
+    o.agg = opts->agg;
+    o.engine = opts->engine;
+    o.workspace = opts->workspace;
+    o.workspace_bytes = opts->workspace_bytes;
+    o.timer = opts->timer;
+  }
+  CHECK_ARG(o.agg == DMV3D_AGG_MEAN || o.agg == DMV3D_AGG_SUM, "bad agg");
+  CHECK_ARG(o.engine >= DMV3D_ENGINE_AUTO && o.engine <= DMV3D_ENGINE_TCGEN05, "bad engine");
   CHECK_ARG(grid_res >= 2 && grid_res <= 2048, "density grid: grid_res must be in [2, 2048]");
   CHECK_ARG(sigma != nullptr, "density grid: sigma is NULL");
   CHECK_ALIGN(sigma, "sigma");
   if (rgb) CHECK_ALIGN(rgb, "rgb");
-  if (!simt_supported(mlp->in_dim, mlp->hidden))
-    return fail(DMV3D_ERR_UNSUPPORTED, "density grid: unsupported (in_dim, hidden)");
+  if (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 255u))
+    return fail(DMV3D_ERR_ALIGNMENT, "opts.workspace is not 256-byte aligned");
   dmv3d_cameras c{};
   c.num_views = c.height = c.width = 1;
   RenderParams P;
-  fill_common(P, triplane, &c, mlp, nullptr);
-  P.agg = agg;
-  P.timer = timer;
+  fill_common(P, triplane, &c, mlp, &o);
+  Engine e;
+  if ((s = pick_engine(triplane, mlp, &o, e)) != DMV3D_OK) return s;
+  if (e == Engine::TC) {
+    P.grid_res = grid_res;
+    P.grid_sigma = sigma;
+    P.grid_rgb = rgb;
+    return cuda_status(launch_render_tc(P, reinterpret_cast<cudaStream_t>(stream)),
+                       "density grid launch");
+  }
+  if (!simt_supported(mlp->in_dim, mlp->hidden))
+    return fail(DMV3D_ERR_UNSUPPORTED, "density grid: unsupported (in_dim, hidden)");
   return cuda_status(launch_density_grid(P, triplane->dtype == DMV3D_BF16,
                                          mlp->dtype == DMV3D_BF16, grid_res, sigma, rgb,
                                          reinterpret_cast<cudaStream_t>(stream)),

@@ -58,6 +58,9 @@ struct RenderParams {
   void *timer;
   // optional Plucker ray map output [V][6][H][W] (row f2), written during a1
   float *plucker;
+  // density grid mode of the tensor-core engine (row f3): G^3 points, x fastest
+  int32_t grid_res;
+  float *grid_sigma, *grid_rgb;
 };
 
 // ---------------------------------------------------------------- a1: rays

@@ -136,7 +136,10 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
   ptx::tmem_st_wait();
 }
 
-template <int NG>
+// GRID = false: the renderer (rays, compositing, DDIM epilogue).  GRID = true: the
+// density grid (row f3): a "patch" is an 8x4x4 block of grid points, decoded in one
+// 128-row tile through the same staged-texel blend + MLP MMAs.
+template <int NG, bool GRID>
 __global__ void __launch_bounds__(128 * NG, 1)
     render_tc_kernel(const __grid_constant__ RenderParams P) {
   extern __shared__ uint8_t smem_raw[];
@@ -206,7 +209,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int v_lo = (int)(P.ray_begin / HW);
   const int v_hi = (int)((P.ray_end - 1) / HW);
   const int PH = (P.H + kPatch - 1) / kPatch, PW = (P.W + kPatch - 1) / kPatch;
-  const int64_t npatch = (int64_t)(v_hi - v_lo + 1) * PH * PW;
+  const int GB[3] = {(P.grid_res + 7) / 8, (P.grid_res + 3) / 4, (P.grid_res + 3) / 4};
+  const int64_t npatch = GRID ? (int64_t)GB[0] * GB[1] * GB[2]
+                              : (int64_t)(v_hi - v_lo + 1) * PH * PW;
   const int slot = tid >> 3, q = tid & 7;
   const int R = P.R;
   const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
@@ -258,17 +263,37 @@ __global__ void __launch_bounds__(128 * NG, 1)
     ptx::bar_sync(bar_id, 128);
     const int64_t patch = sh->patch[g];
     if (patch >= npatch) break;
-    const int v = v_lo + (int)(patch / ((int64_t)PH * PW));
-    const int prem = (int)(patch % ((int64_t)PH * PW));
-    const int i = (prem / PW) * kPatch + (slot >> 2);
-    const int j = (prem % PW) * kPatch + (slot & 3);
-    const int64_t r = (int64_t)v * HW + (int64_t)i * P.W + j;
-    const bool pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
+    int v = 0, i = 0, j = 0;
+    int64_t r = 0;
+    bool pix;
     Ray ray;
     ray.hit = false;
     ray.t_near = ray.t_far = 0.0f;
-    if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
-    if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
+    float gp[3] = {0.f, 0.f, 0.f};  // GRID: this row's grid point
+    if constexpr (GRID) {
+      const int G = P.grid_res;
+      const int bx = (int)(patch % GB[0]), by = (int)((patch / GB[0]) % GB[1]),
+                bz = (int)(patch / ((int64_t)GB[0] * GB[1]));
+      const int id3[3] = {bx * 8 + (tid & 7), by * 4 + ((tid >> 3) & 3), bz * 4 + (tid >> 5)};
+      pix = id3[0] < G && id3[1] < G && id3[2] < G;
+      r = ((int64_t)id3[2] * G + id3[1]) * G + id3[0];
+      const float gm1 = __int2float_rn(G - 1);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float s = __fdiv_rn(__int2float_rn(id3[a]), gm1);
+        gp[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
+      }
+      ray.hit = pix;
+    } else {
+      v = v_lo + (int)(patch / ((int64_t)PH * PW));
+      const int prem = (int)(patch % ((int64_t)PH * PW));
+      i = (prem / PW) * kPatch + (slot >> 2);
+      j = (prem % PW) * kPatch + (slot & 3);
+      r = (int64_t)v * HW + (int64_t)i * P.W + j;
+      pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
+      if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
+      if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
+    }
     bool alive = pix && ray.hit;
     const float delta = alive ? sample_delta(ray, P.N) : 0.0f;
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
@@ -295,9 +320,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ix[0] = ix[1] = ix[2] = 0;
       fr[0] = fr[1] = fr[2] = 0.f;
       if (sv) {
-        const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
         float p[3];
-        sample_p(ray, sample_t(ray, delta, k, u), p);
+        if constexpr (GRID) {
+          p[0] = gp[0];
+          p[1] = gp[1];
+          p[2] = gp[2];
+        } else {
+          const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
+          sample_p(ray, sample_t(ray, delta, k, u), p);
+        }
 #pragma unroll
         for (int a = 0; a < 3; ++a) texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, ix[a], fr[a]);
       }
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
       // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
       const int k1 = k0 + kChunk;
-      const bool nxt = k1 < P.N;
+      const bool nxt = !GRID && k1 < P.N;
       if (nxt) prefetch(k1, alive);
 
       // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
@@ -419,6 +450,19 @@ __global__ void __launch_bounds__(128 * NG, 1)
         c2 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[3]))) - P.weps;
         n_samples++;
       }
+      if constexpr (GRID) {
+        if (sv) {
+          const int64_t n3 = (int64_t)P.grid_res * P.grid_res * P.grid_res;
+          P.grid_sigma[r] = sigma;
+          if (P.grid_rgb) {
+            P.grid_rgb[r] = c0;
+            P.grid_rgb[n3 + r] = c1;
+            P.grid_rgb[2 * n3 + r] = c2;
+          }
+        }
+        have = false;
+        continue;
+      }
       // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
       const float tau = sv ? sigma * delta : 0.0f;
       float S = tau;
@@ -449,7 +493,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       acc1 += __shfl_xor_sync(0xffffffffu, acc1, s, kChunk);
       acc2 += __shfl_xor_sync(0xffffffffu, acc2, s, kChunk);
     }
-    if (pix && q < 3) ray_epilogue(P, v, i, j, q, q == 0 ? acc0 : (q == 1 ? acc1 : acc2), T);
+    if (!GRID && pix && q < 3) ray_epilogue(P, v, i, j, q, q == 0 ? acc0 : (q == 1 ? acc1 : acc2), T);
   }
 
   if (P.counters) {
@@ -476,20 +520,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
 }
 
 // ------------------------------------------------------------------ launch
-template <int NG>
+template <int NG, bool GRID>
 static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
   const size_t s1 = tc_smem_bytes<NG>(P.L);
-  cudaError_t e = cudaFuncSetAttribute(render_tc_kernel<NG>,
+  cudaError_t e = cudaFuncSetAttribute(render_tc_kernel<NG, GRID>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
   if (e != cudaSuccess) return e;
   int grid = sms;
   if ((int64_t)grid * NG > npatch) grid = (int)((npatch + NG - 1) / NG);
-  render_tc_kernel<NG><<<grid, 128 * NG, s1, st>>>(P);
+  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P);
   return cudaGetLastError();
 }
 
+// P.grid_res > 0 selects the density-grid mode (row f3)
 cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
-  if (P0.ray_end <= P0.ray_begin) return cudaSuccess;
+  const bool grid_mode = P0.grid_res > 0;
+  if (!grid_mode && P0.ray_end <= P0.ray_begin) return cudaSuccess;
   if (!P0.ws) return cudaErrorInvalidValue;
   RenderParams P = P0;
   uint8_t *ws = static_cast<uint8_t *>(P.ws);
@@ -513,12 +559,18 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
-  const int64_t HW = (int64_t)P.H * P.W;
-  const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
-  const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
+  const bool ng4 = tc_smem_bytes<4>(P.L) <= kSmemLimit;
   timer_begin(P.timer, st);
-  e = (tc_smem_bytes<4>(P.L) <= kSmemLimit) ? launch_k1<4>(P, sms, npatch, st)
-                                            : launch_k1<2>(P, sms, npatch, st);
+  if (grid_mode) {
+    const int Gr = P.grid_res;
+    const int64_t nb = (int64_t)((Gr + 7) / 8) * ((Gr + 3) / 4) * ((Gr + 3) / 4);
+    e = ng4 ? launch_k1<4, true>(P, sms, nb, st) : launch_k1<2, true>(P, sms, nb, st);
+  } else {
+    const int64_t HW = (int64_t)P.H * P.W;
+    const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
+    const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
+    e = ng4 ? launch_k1<4, false>(P, sms, npatch, st) : launch_k1<2, false>(P, sms, npatch, st);
+  }
   timer_end(P.timer, st);
   return e;
 }

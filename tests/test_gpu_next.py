@@ -50,19 +50,23 @@ def test_plucker_emitted_by_the_renderer(engine, dtype):
     assert torch.equal(pl, ref)
 
 
-@pytest.mark.parametrize("G,dtype", [(9, "f32"), (20, "f32"), (33, "bf16")])
-def test_density_grid_matches_oracle(G, dtype):
+@pytest.mark.parametrize("G,dtype,engine", [(9, "f32", "simt"), (20, "f32", "simt"),
+                                            (33, "bf16", "simt"), (33, "bf16", "tcgen05"),
+                                            (70, "bf16", "tcgen05")])
+def test_density_grid_matches_oracle(G, dtype, engine):
     tp = wl.blob_triplane(12, 32, seed=4)
     m = wl.blob_mlp(32, 64, 4, seed=5)
     if dtype == "bf16":
         tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
     dt = torch.bfloat16 if dtype == "bf16" else torch.float32
     sigma, rgb = api.dmv3d_density_grid(torch.from_numpy(tp).cuda().to(dt),
-                                        api.DeviceMLP.from_host(m, dtype), G)
+                                        api.DeviceMLP.from_host(m, dtype), G, engine=engine)
     osig, orgb = oracle.density_grid(tp, m, G)
     s = sigma.cpu().numpy()
-    assert np.max(np.abs(s - osig) / np.maximum(1.0, osig)) < 1e-5
-    assert np.max(np.abs(rgb.cpu().numpy() - orgb)) < 1e-5
+    # fp32 engine: 1e-5; tensor-core engine (fp16 MMAs): the 2e-2 bar on the decoded values
+    tol = 1e-5 if engine == "simt" else 2e-2
+    assert np.max(np.abs(s - osig) / np.maximum(1.0, osig)) < tol
+    assert np.max(np.abs(rgb.cpu().numpy() - orgb)) < tol
     # the blob is a ball: the level set sigma = 1 encloses the centre, not the corners
     c = G // 2
     assert s[c, c, c] > 1.0 and s[0, 0, 0] < 1.0

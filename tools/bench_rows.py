@@ -80,16 +80,25 @@ def main():
     mlp = api.DeviceMLP.from_host(w.mlp, "bf16", dev)
     G = 128
 
-    def f3(timer):
-        api.dmv3d_density_grid(tp, mlp, G, timer=timer)
-    ms = timed(f3, args.reps, flush)
-    pts = G ** 3
-    fl = pts * (27136 + 1920) / (ms / 1e3) / 1e12
-    out.append({"row": "f3 density grid", "metric": "points/s", "value": pts / (ms / 1e3),
-                "kernel_ms": ms, "config": "128^3 grid, C=80, MLP 80-64-64-64-4, bf16 storage, fp32 SIMT",
-                "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
-                             "frac": fl / FP32_PEAK,
-                             "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per point"}})
+    for engine in ("simt", "tcgen05"):
+        def f3(timer):
+            api.dmv3d_density_grid(tp, mlp, G, timer=timer, engine=engine)
+        ms = timed(f3, args.reps, flush)
+        pts = G ** 3
+        if engine == "simt":
+            fl = pts * (27136 + 1920) / (ms / 1e3) / 1e12
+            roof = {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
+                    "frac": fl / FP32_PEAK,
+                    "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per point"}
+        else:
+            fl = pts * 27136 / (ms / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": fl, "peak": pk.get("bf16_tflops", 1590.0),
+                    "unit": "TFLOP/s", "frac": fl / pk.get("bf16_tflops", 1590.0),
+                    "algorithmic": "27,136 MLP FLOP per point"}
+        out.append({"row": f"f3 density grid ({engine})", "metric": "points/s",
+                    "value": pts / (ms / 1e3), "kernel_ms": ms,
+                    "config": f"128^3 grid, C=80, MLP 80-64-64-64-4, bf16 storage, {engine}",
+                    "roofline": roof})
 
     # f1: renderer backward, 8 views of 128^2 training crops, N = 128
     cams = wl.concat_cameras(wl.input_cameras(128, 128, 4), wl.novel_cameras(128, 128, 4))
