@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       par = chunk_ctr & 1;
       ++chunk_ctr;
       const int k = kk + q;
-      const bool sv = spec_alive && k < P.N;
+      const bool sv = spec_alive && (GRID || k < P.N);  // GRID: one point per row
       ix[0] = ix[1] = ix[2] = 0;
       fr[0] = fr[1] = fr[2] = 0.f;
       if (sv) {
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     if (have) prefetch(0, alive);
     for (int k0 = 0; have;) {
       const int k = k0 + q;
-      const bool sv = alive && k < P.N;
+      const bool sv = alive && (GRID || k < P.N);
       const int *bb = sh->bbox[g][par];
       const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;

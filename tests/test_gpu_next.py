@@ -65,6 +65,7 @@ def test_density_grid_matches_oracle(G, dtype, engine):
     s = sigma.cpu().numpy()
     # fp32 engine: 1e-5; tensor-core engine (fp16 MMAs): the 2e-2 bar on the decoded values
     tol = 1e-5 if engine == "simt" else 2e-2
+    assert np.all(s > 0) and np.all(np.isfinite(s))  # softplus > 0: every point written
     assert np.max(np.abs(s - osig) / np.maximum(1.0, osig)) < tol
     assert np.max(np.abs(rgb.cpu().numpy() - orgb)) < tol
     # the blob is a ball: the level set sigma = 1 encloses the centre, not the corners
