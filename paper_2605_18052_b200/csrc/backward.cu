@@ -21,7 +21,6 @@
 namespace dmv3d {
 
 constexpr int kBwThreads = 128;
-constexpr int kBwStride = kBwThreads + 1;  // padded rows: column reads are conflict-free
 
 template <int K, int HD>
 __device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const MlpSmem &m,
@@ -64,7 +63,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
   scratch = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(scratch) + 15) & ~uintptr_t(15));
   const int L = P.L;
   const int rows = K + (L - 1) * HD;
-  float *dstage = scratch + rows * kBwStride;  // [warps][32 samples][HD]
+  float *dstage = scratch + rows * kBwThreads;  // [warps][32 samples][HD]
   __syncthreads();
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -100,7 +99,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         sample_p(ray, sample_t(ray, delta, k, u), p);
         float x[K];
         gather_features<BF16, K>(P, p, x);
-        mlp_decode<K, HD>(P, m, x, col, kBwStride, sigma, c);
+        mlp_decode<K, HD>(P, m, x, col, kBwThreads, sigma, c);
       }
       const float tau = valid ? sigma * delta : 0.0f;
       float S = tau;
@@ -137,10 +136,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         float x[K];
         gather_features<BF16, K>(P, p, x);
 #pragma unroll
-        for (int c = 0; c < K; ++c) col[c * kBwStride] = x[c];
-        mlp_forward_store<K, HD>(P, m, col, kBwStride, o4);
+        for (int c = 0; c < K; ++c) col[c * kBwThreads] = x[c];
+        mlp_forward_store<K, HD>(P, m, col, kBwThreads, o4);
       } else {
-        for (int rr = 0; rr < rows; ++rr) col[rr * kBwStride] = 0.0f;
+        for (int rr = 0; rr < rows; ++rr) col[rr * kBwThreads] = 0.0f;
       }
       const float z0 = o4[0] + P.dshift;
       const float sigma = valid ? (log1pf(expf(-fabsf(z0))) + fmaxf(z0, 0.0f)) : 0.0f;
@@ -204,7 +203,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           }
           if (bsum != 0.0f) atomicAdd(Gp.db[l] + q, bsum);
           for (int ii = 0; ii < in; ++ii) {
-            const float *hr = wcol + (hrow + ii) * kBwStride;
+            const float *hr = wcol + (hrow + ii) * kBwThreads;
             float sum = 0.0f;
 #pragma unroll
             for (int s = 0; s < 32; ++s) sum += dq[s] * hr[s];
@@ -219,55 +218,28 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 #pragma unroll
             for (int q = 0; q < HD; ++q)
               if (q < out) dh += m.W[l][q * in + ii] * d[q];
-            const float h = col[(hrow + ii) * kBwStride];
-            col[(hrow + ii) * kBwStride] = h > 0.0f ? dh : 0.0f;
+            const float h = col[(hrow + ii) * kBwThreads];
+            col[(hrow + ii) * kBwThreads] = h > 0.0f ? dh : 0.0f;
           }
 #pragma unroll
-          for (int q = 0; q < HD; ++q) d[q] = col[(hrow + q) * kBwStride];
-        } else {
-          // dL/dh0 = W0^T d into this lane's (now free) h0 rows; the sample's cells
-          // into the warp's staging area (offset of corner (iy, ix), fx, fy per plane)
-          for (int cc = 0; cc < K; ++cc) {
-            float dh = 0.0f;
-#pragma unroll
-            for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + cc] * d[q];
-            col[cc * kBwStride] = valid ? dh : 0.0f;
-          }
-          int *cell_off = reinterpret_cast<int *>(dst);  // [3][32] int + [3][32][2] float
-          float *cell_f = dst + 96;
+          for (int q = 0; q < HD; ++q) d[q] = col[(hrow + q) * kBwThreads];
+        } else if (valid) {
+          // dL/dh0 -> the 12 bilinear corners of the three planes
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
             const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext);
-            cell_off[pl * 32 + lane] = valid ? (int)cell.off : -1;
-            cell_f[(pl * 32 + lane) * 2] = cell.fx;
-            cell_f[(pl * 32 + lane) * 2 + 1] = cell.fy;
-          }
-          __syncwarp();
-          // channel-parallel scatter to the 12 bilinear corners: lanes own channels,
-          // walk the 32 samples in ray order and merge runs that hit the same texel
-          // before one coalesced atomic per (texel, channel)
-          const int rowC = P.R * P.C;
-          for (int e = 0; e < 12; ++e) {
-            const int pl = e >> 2, dx = e & 1, dy = (e >> 1) & 1;
-            const int corner = dy * rowC + dx * P.C;
-            for (int c0 = 0; c0 < K; c0 += 32) {
-              const int cc = c0 + lane;
-              int cur = -1;
-              float accv = 0.0f;
-              for (int s = 0; s < 32; ++s) {
-                const int off = cell_off[pl * 32 + s];
-                if (off < 0) continue;
-                const float fx = cell_f[(pl * 32 + s) * 2], fy = cell_f[(pl * 32 + s) * 2 + 1];
-                const float wgt = (dx ? fx : 1.0f - fx) * (dy ? fy : 1.0f - fy) * scale;
-                const int key = off + corner;
-                if (key != cur) {
-                  if (cur >= 0 && cc < K && accv != 0.0f) atomicAdd(Gp.dF + cur + cc, accv);
-                  cur = key;
-                  accv = 0.0f;
-                }
-                if (cc < K) accv += wgt * wcol[cc * kBwStride + s];
-              }
-              if (cur >= 0 && cc < K && accv != 0.0f) atomicAdd(Gp.dF + cur + cc, accv);
+            const float gx = 1.0f - cell.fx, gy = 1.0f - cell.fy;
+            const float wc[4] = {gx * gy * scale, cell.fx * gy * scale, gx * cell.fy * scale,
+                                 cell.fx * cell.fy * scale};
+            const int64_t rowC = (int64_t)P.R * P.C;
+            const int64_t off[4] = {cell.off, cell.off + P.C, cell.off + rowC, cell.off + rowC + P.C};
+            for (int cc = 0; cc < K; ++cc) {
+              float dh = 0.0f;
+#pragma unroll
+              for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + cc] * d[q];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (wc[e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wc[e] * dh);
             }
           }
         }
@@ -298,7 +270,7 @@ static cudaError_t bw_launch(Fn fn, size_t smem, int64_t rays, cudaStream_t st, 
 
 size_t backward_smem_bytes(int K, int HD, int L) {
   const size_t mlp = (size_t)HD * K + (size_t)(L - 2) * HD * HD + 4 * HD + (size_t)(L - 1) * HD + 4;
-  return (mlp + 4 + (size_t)(K + (L - 1) * HD) * kBwStride + (size_t)4 * 32 * HD) * 4;
+  return (mlp + 4 + (size_t)(K + (L - 1) * HD) * kBwThreads + (size_t)4 * 32 * HD) * 4;
 }
 
 #define DMV3D_BW_SHAPES(X) \
