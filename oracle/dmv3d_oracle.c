@@ -188,35 +188,62 @@ void orc_texel_coord(float q, float lo, float hi, int32_t R, int32_t *i0, float 
   *f = px - (float)ix;
 }
 
+/* Row f4 variant: half-pixel texel centres with zero padding (the        */
+/* convention of grid_sample(align_corners=False, padding_mode='zeros')):  */
+/* px = ((q - lo)/(hi - lo)) R - 1/2, i0 = floor(px) in [-1, R-1], no      */
+/* clamp; texels outside the plane read as 0.                              */
+void orc_texel_coord_halfpixel(float q, float lo, float hi, int32_t R, int32_t *i0, float *f) {
+  float ext = hi - lo;
+  float s = (q - lo) / ext;
+  float a = s * (float)R;
+  float px = a - 0.5f;
+  int32_t ix = (int32_t)floorf(px);
+  *i0 = ix;
+  *f = px - (float)ix;
+}
+
+static void texel_coord_mode(const orc_triplane *tp, int axis, float q, int32_t *i0, float *f) {
+  if (tp->sample_mode == ORC_SAMPLE_HALFPIXEL_ZEROS)
+    orc_texel_coord_halfpixel(q, tp->aabb_min[axis], tp->aabb_max[axis], tp->res, i0, f);
+  else
+    orc_texel_coord(q, tp->aabb_min[axis], tp->aabb_max[axis], tp->res, i0, f);
+}
+
+/* texel (row, col) of plane pl, or NULL outside the plane (zero padding) */
+static const double *texel(const orc_triplane *tp, int pl, int32_t row, int32_t col) {
+  const int32_t R = tp->res;
+  if (row < 0 || row >= R || col < 0 || col >= R) return NULL;
+  return tp->data + (((size_t)pl * R + row) * R + col) * tp->channels;
+}
+
 /* ------------------------------------------------------------------ */
 /* Triplane NeRF features (A2-A4): planes XY,   */
 /* XZ, YZ; plane (a,b): column <- axis a, row <- axis b; bilinear       */
-/* interpolation of the 4 texels; mean (or sum) over the 3 planes.      */
+/* interpolation of the 4 texels; mean (or sum) over the 3 planes, or   */
+/* their concatenation (row f4).                                        */
 /* ------------------------------------------------------------------ */
 static const int PLANE_AXES[3][2] = {{0, 1}, {0, 2}, {1, 2}};
 
 void orc_point_features(const orc_triplane *tp, int32_t agg, const float p[3], double *out) {
-  const int32_t R = tp->res, C = tp->channels;
-  for (int32_t c = 0; c < C; ++c) out[c] = 0.0;
+  const int32_t C = tp->channels;
+  const int32_t K = agg == ORC_AGG_CONCAT ? 3 * C : C;
+  for (int32_t c = 0; c < K; ++c) out[c] = 0.0;
   for (int pl = 0; pl < 3; ++pl) {
     int a = PLANE_AXES[pl][0], b = PLANE_AXES[pl][1];
     int32_t ix, iy;
     float fxf, fyf;
-    orc_texel_coord(p[a], tp->aabb_min[a], tp->aabb_max[a], R, &ix, &fxf);
-    orc_texel_coord(p[b], tp->aabb_min[b], tp->aabb_max[b], R, &iy, &fyf);
+    texel_coord_mode(tp, a, p[a], &ix, &fxf);
+    texel_coord_mode(tp, b, p[b], &iy, &fyf);
     double fx = (double)fxf, fy = (double)fyf;
-    double w00 = (1.0 - fx) * (1.0 - fy);
-    double w01 = fx * (1.0 - fy);
-    double w10 = (1.0 - fx) * fy;
-    double w11 = fx * fy;
-    const double *P = tp->data + (size_t)pl * R * R * C;
-    const double *t00 = P + ((size_t)iy * R + ix) * C;
-    const double *t01 = P + ((size_t)iy * R + ix + 1) * C;
-    const double *t10 = P + ((size_t)(iy + 1) * R + ix) * C;
-    const double *t11 = P + ((size_t)(iy + 1) * R + ix + 1) * C;
+    const double w[4] = {(1.0 - fx) * (1.0 - fy), fx * (1.0 - fy), (1.0 - fx) * fy, fx * fy};
+    const double *t[4] = {texel(tp, pl, iy, ix), texel(tp, pl, iy, ix + 1),
+                          texel(tp, pl, iy + 1, ix), texel(tp, pl, iy + 1, ix + 1)};
+    double *dst = out + (agg == ORC_AGG_CONCAT ? pl * C : 0);
     for (int32_t c = 0; c < C; ++c) {
-      double v = w00 * t00[c] + w01 * t01[c] + w10 * t10[c] + w11 * t11[c];
-      out[c] += v;
+      double v = 0.0;
+      for (int e = 0; e < 4; ++e)
+        if (t[e]) v += w[e] * t[e][c];
+      dst[c] += v;
     }
   }
   if (agg == ORC_AGG_MEAN)
@@ -269,7 +296,7 @@ void orc_mlp_decode(const orc_mlp *mlp, const double *h0, double *sigma, double 
 
 void orc_decode_point(const orc_triplane *tp, const orc_mlp *mlp, int32_t agg,
                       const float p[3], double out[4]) {
-  double *h0 = (double *)malloc(sizeof(double) * tp->channels);
+  double *h0 = (double *)malloc(sizeof(double) * 3 * tp->channels); /* concat: 3C */
   orc_point_features(tp, agg, p, h0);
   double sigma, rgb[3];
   orc_mlp_decode(mlp, h0, &sigma, rgb);
@@ -333,7 +360,7 @@ void orc_render_ray(const orc_triplane *tp, const orc_cameras *cams, const orc_m
   const int32_t N = opts->samples_per_ray;
   const double delta = (double)((tf - tn) / (float)N);
   double T = 1.0, acc[3] = {0.0, 0.0, 0.0};
-  double *h0 = (double *)malloc(sizeof(double) * tp->channels);
+  double *h0 = (double *)malloc(sizeof(double) * 3 * tp->channels); /* concat: 3C */
   for (int32_t k = 0; k < N; ++k) {
     float tk, p[3];
     orc_sample_point(o, d, tn, tf, N, k, opts->jitter, opts->seed, r, &tk, p);
@@ -459,15 +486,17 @@ void orc_render_ray_backward(const orc_triplane *tp, const orc_cameras *cams,
       const int a = PLANE_AXES[pl][0], b = PLANE_AXES[pl][1];
       int32_t ix, iy;
       float fxf, fyf;
-      orc_texel_coord(pts[3 * k + a], tp->aabb_min[a], tp->aabb_max[a], R, &ix, &fxf);
-      orc_texel_coord(pts[3 * k + b], tp->aabb_min[b], tp->aabb_max[b], R, &iy, &fyf);
+      texel_coord_mode(tp, a, pts[3 * k + a], &ix, &fxf);
+      texel_coord_mode(tp, b, pts[3 * k + b], &iy, &fyf);
       const double fx = fxf, fy = fyf;
       const double wc[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
-      const size_t off[4] = {((size_t)(pl * R + iy) * R + ix) * C, ((size_t)(pl * R + iy) * R + ix + 1) * C,
-                             ((size_t)(pl * R + iy + 1) * R + ix) * C,
-                             ((size_t)(pl * R + iy + 1) * R + ix + 1) * C};
-      for (int e = 0; e < 4; ++e)
-        for (int32_t c = 0; c < C; ++c) dF[off[e] + c] += scale * wc[e] * dh[c];
+      const int32_t rr[4] = {iy, iy, iy + 1, iy + 1}, cc4[4] = {ix, ix + 1, ix, ix + 1};
+      const double *g = dh + (opts->agg == ORC_AGG_CONCAT ? pl * C : 0);
+      for (int e = 0; e < 4; ++e) {
+        if (rr[e] < 0 || rr[e] >= R || cc4[e] < 0 || cc4[e] >= R) continue;  /* zero padding */
+        const size_t off = ((size_t)(pl * R + rr[e]) * R + cc4[e]) * C;
+        for (int32_t c = 0; c < C; ++c) dF[off + c] += scale * wc[e] * g[c];
+      }
     }
   }
 #undef H_IN

@@ -31,6 +31,9 @@ extern "C" {
 
 #define ORC_AGG_MEAN 0
 #define ORC_AGG_SUM 1
+#define ORC_AGG_CONCAT 2
+#define ORC_SAMPLE_ALIGN_CORNERS 0
+#define ORC_SAMPLE_HALFPIXEL_ZEROS 1
 #define ORC_ACT_RELU 0
 #define ORC_ACT_SILU 1
 #define ORC_ACT_SOFTPLUS 2
@@ -39,6 +42,7 @@ typedef struct {
   int32_t res, channels;
   const double *data; /* [3][res][res][channels] (bf16/fp32 inputs upcast exactly) */
   float aabb_min[3], aabb_max[3];
+  int32_t sample_mode; /* ORC_SAMPLE_* (A3; half-pixel + zero padding is row f4) */
 } orc_triplane;
 
 typedef struct {
@@ -84,6 +88,7 @@ void orc_sample_point(const float o[3], const float d[3], float t_near, float t_
 
 /* fp32 texel index/fraction for coordinate q on an axis [lo,hi] (align corners). */
 void orc_texel_coord(float q, float lo, float hi, int32_t R, int32_t *i0, float *f);
+void orc_texel_coord_halfpixel(float q, float lo, float hi, int32_t R, int32_t *i0, float *f);
 
 /* aggregated triplane feature at point p, fp64 out [K] (C1 step 4). */
 void orc_point_features(const orc_triplane *tp, int32_t agg, const float p[3], double *out);

@@ -17,7 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dmv3d_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-AGG_MEAN, AGG_SUM = 0, 1
+AGG_MEAN, AGG_SUM, AGG_CONCAT = 0, 1, 2
+SAMPLE_ALIGN_CORNERS, SAMPLE_HALFPIXEL_ZEROS = 0, 1
 
 
 def build(force: bool = False) -> str:
@@ -32,7 +33,8 @@ def build(force: bool = False) -> str:
 
 class _Triplane(ct.Structure):
     _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("data", ct.POINTER(ct.c_double)),
-                ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3)]
+                ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3),
+                ("sample_mode", ct.c_int32)]
 
 
 class _MLP(ct.Structure):
@@ -114,10 +116,10 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def _triplane(tp, keep, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+def _triplane(tp, keep, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1), sample_mode=0):
     tp = keep(_f64(tp))  # fp32 / bf16-valued inputs upcast exactly
     s = _Triplane(tp.shape[1], tp.shape[3], _dp(tp), (ct.c_float * 3)(*aabb_min),
-                  (ct.c_float * 3)(*aabb_max))
+                  (ct.c_float * 3)(*aabb_max), sample_mode)
     return s
 
 
@@ -188,11 +190,11 @@ def plucker(cams, ray_ids):
 
 
 def render_backward(tp, cams, m, N, grad_rgb, grad_alpha=None, agg=AGG_MEAN, jitter=0, seed=0,
-                    bg=(1.0, 1.0, 1.0)):
+                    bg=(1.0, 1.0, 1.0), sample_mode=0):
     """Gradients of L = sum(grad_rgb * rgb) + sum(grad_alpha * alpha) w.r.t. the triplane
     and the MLP (row f1) -> (dF [3,R,R,C], [dW_l], [db_l]), fp64."""
     keep = _Keep()
-    t = _triplane(tp, keep)
+    t = _triplane(tp, keep, sample_mode=sample_mode)
     mm = _mlp(m, keep)
     c = _cams(cams, keep)
     o = _opts(N, agg, jitter, seed, bg)
@@ -265,21 +267,25 @@ def sample_point(o, d, t_near, t_far, N, k, jit=0, seed=0, r=0):
     return np.float32(t.value), p
 
 
-def texel_coord(q, lo, hi, R):
+def texel_coord(q, lo, hi, R, sample_mode=0):
     i0 = ct.c_int32()
     f = ct.c_float()
-    lib().orc_texel_coord(float(q), float(lo), float(hi), R, ct.byref(i0), ct.byref(f))
+    fn = lib().orc_texel_coord_halfpixel if sample_mode == 1 else lib().orc_texel_coord
+    fn.argtypes = [ct.c_float, ct.c_float, ct.c_float, ct.c_int32, ct.POINTER(ct.c_int32),
+                   ct.POINTER(ct.c_float)]
+    fn(float(q), float(lo), float(hi), R, ct.byref(i0), ct.byref(f))
     return i0.value, np.float32(f.value)
 
 
-def point_features(tp, points, agg=AGG_MEAN):
+def point_features(tp, points, agg=AGG_MEAN, sample_mode=0):
     keep = _Keep()
-    t = _triplane(tp, keep)
+    t = _triplane(tp, keep, sample_mode=sample_mode)
     pts = _f32(points).reshape(-1, 3)
-    out = np.zeros((len(pts), tp.shape[3]), np.float64)
+    K = tp.shape[3] * (3 if agg == AGG_CONCAT else 1)
+    out = np.zeros((len(pts), K), np.float64)
     for q in range(len(pts)):
         p = np.ascontiguousarray(pts[q])
-        row = np.zeros(tp.shape[3], np.float64)
+        row = np.zeros(K, np.float64)
         lib().orc_point_features(ct.byref(t), agg, _fp(p), _dp(row))
         out[q] = row
     return out
@@ -299,9 +305,9 @@ def mlp_decode(m, h0):
     return out
 
 
-def decode_points(tp, m, points, agg=AGG_MEAN):
+def decode_points(tp, m, points, agg=AGG_MEAN, sample_mode=0):
     keep = _Keep()
-    t = _triplane(tp, keep)
+    t = _triplane(tp, keep, sample_mode=sample_mode)
     mm = _mlp(m, keep)
     pts = _f32(points).reshape(-1, 3)
     out = np.zeros((len(pts), 4), np.float64)
@@ -314,10 +320,10 @@ def decode_points(tp, m, points, agg=AGG_MEAN):
 
 
 def render_rays(tp, cams, m, N, ray_ids, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0, 1.0, 1.0),
-                threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+                threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1), sample_mode=0):
     """Render selected ray ids -> rgb [n,3], alpha [n] (fp64)."""
     keep = _Keep()
-    t = _triplane(tp, keep, aabb_min, aabb_max)
+    t = _triplane(tp, keep, aabb_min, aabb_max, sample_mode)
     mm = _mlp(m, keep)
     c = _cams(cams, keep)
     o = _opts(N, agg, jitter, seed, bg)
@@ -331,10 +337,10 @@ def render_rays(tp, cams, m, N, ray_ids, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0
 
 
 def render_views(tp, cams, m, N, agg=AGG_MEAN, jitter=0, seed=0, bg=(1.0, 1.0, 1.0), threads=0,
-                 aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+                 aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1), sample_mode=0):
     """Render all views -> rgb [V,3,H,W], alpha [V,H,W] (fp64)."""
     keep = _Keep()
-    t = _triplane(tp, keep, aabb_min, aabb_max)
+    t = _triplane(tp, keep, aabb_min, aabb_max, sample_mode)
     mm = _mlp(m, keep)
     c = _cams(cams, keep)
     o = _opts(N, agg, jitter, seed, bg)

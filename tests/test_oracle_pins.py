@@ -435,6 +435,43 @@ def test_density_grid_on_texel_lattice():
     assert np.max(np.abs(rgb.reshape(3, -1).T - want[:, 1:])) < 1e-12
 
 
+# ----------------------------------------------------------------------------- f4 variants
+def test_halfpixel_zero_padding_matches_grid_sample():
+    """Row f4: half-pixel texel centres with zero padding are exactly
+    grid_sample(align_corners=False, padding_mode='zeros') on each plane."""
+    R, C = 7, 5
+    tp = wl.random_triplane(R, C, seed=11)
+    pts = np.random.default_rng(11).uniform(-1, 1, (400, 3)).astype(np.float32)
+    got = oracle.point_features(tp, pts, oracle.AGG_SUM, sample_mode=oracle.SAMPLE_HALFPIXEL_ZEROS)
+    t = torch.from_numpy(tp.astype(np.float64))
+    p = torch.from_numpy(pts.astype(np.float64))
+    want = 0
+    for pl, (a, b) in enumerate([(0, 1), (0, 2), (1, 2)]):
+        img = t[pl].permute(2, 0, 1)[None]
+        grid = torch.stack([p[:, a], p[:, b]], -1)[None, None]
+        want = want + F.grid_sample(img, grid, mode="bilinear", padding_mode="zeros",
+                                    align_corners=False)[0, :, 0, :].T
+    # fp32 fractions (reading A3): |df| <= ~R*2^-24 per axis, x texel deltas, x3 planes summed
+    assert np.max(np.abs(got - want.numpy())) < 6e-6
+    # near the faces the half-pixel mode fades to zero, unlike align-corners
+    i0, f = oracle.texel_coord(-1.0, -1.0, 1.0, R, sample_mode=1)
+    assert (i0, f) == (-1, 0.5)
+
+
+def test_concat_aggregation_stacks_the_planes():
+    """Row f4: concat aggregation (A4 alternative) = [f_XY, f_XZ, f_YZ], each the
+    align-corners bilinear lookup of its plane; the mean is their average."""
+    R, C = 9, 4
+    tp = wl.random_triplane(R, C, seed=12)
+    pts = np.random.default_rng(12).uniform(-1, 1, (300, 3)).astype(np.float32)
+    cat = oracle.point_features(tp, pts, oracle.AGG_CONCAT)
+    assert cat.shape == (300, 3 * C)
+    mean = torch_features(tp, pts, oracle.AGG_MEAN)
+    assert np.max(np.abs((cat[:, :C] + cat[:, C:2 * C] + cat[:, 2 * C:]) / 3 - mean)) < 2e-6
+    single = torch_features(np.stack([tp[1], tp[1], tp[1]]), pts, oracle.AGG_SUM)  # not the XZ axes
+    assert np.max(np.abs(cat[:, C:2 * C] - single / 3)) > 1e-3  # planes are not interchangeable
+
+
 # ----------------------------------------------------------------------------- f4 in-kernel noise
 def test_in_kernel_noise_is_standard_normal():
     """Row f4: the counter-based DDIM noise is N(0,1): Kolmogorov-Smirnov distance to
@@ -449,14 +486,15 @@ def test_in_kernel_noise_is_standard_normal():
 
 
 # ----------------------------------------------------------------------------- f1 backward
-@pytest.mark.parametrize("act,agg", [(2, oracle.AGG_MEAN), (1, oracle.AGG_SUM), (0, oracle.AGG_MEAN)])
-def test_render_backward_matches_central_differences(act, agg):
+@pytest.mark.parametrize("act,agg,mode", [(2, oracle.AGG_MEAN, 0), (1, oracle.AGG_SUM, 0),
+                                          (0, oracle.AGG_MEAN, 0), (2, oracle.AGG_CONCAT, 1)])
+def test_render_backward_matches_central_differences(act, agg, mode):
     """Row f1 ("differentiable volume rendering"): the oracle's analytic
     gradients equal central finite differences of the oracle's own forward render,
     (L(x+h) - L(x-h)) / 2h with h = 1e-6 on fp64 inputs (SPEC.md:112 methodology)."""
     rng = np.random.default_rng(act)
     tp = rng.normal(0, 0.8, (3, 5, 5, 4))
-    m = wl.random_mlp(4, 8, 3, seed=act)
+    m = wl.random_mlp(12 if agg == oracle.AGG_CONCAT else 4, 8, 3, seed=act)
     m = wl.MLP([w.astype(np.float64) for w in m.weights], [b.astype(np.float64) for b in m.biases],
                act, 0.3, 0.01)
     cams = wl.input_cameras(4, 4, 2)
@@ -465,10 +503,12 @@ def test_render_backward_matches_central_differences(act, agg):
     gA = rng.normal(size=(2, 4, 4))
 
     def loss(tp_, m_):
-        rgb, alpha = oracle.render_views(tp_, cams, m_, N, agg=agg, bg=(0.3, 0.6, 0.9), threads=1)
+        rgb, alpha = oracle.render_views(tp_, cams, m_, N, agg=agg, bg=(0.3, 0.6, 0.9), threads=1,
+                                         sample_mode=mode)
         return float(np.sum(g * rgb) + np.sum(gA * alpha))
 
-    dF, dW, db = oracle.render_backward(tp, cams, m, N, g, gA, agg=agg, bg=(0.3, 0.6, 0.9))
+    dF, dW, db = oracle.render_backward(tp, cams, m, N, g, gA, agg=agg, bg=(0.3, 0.6, 0.9),
+                                        sample_mode=mode)
     h = 1e-6
     flat = np.argsort(-np.abs(dF).ravel())[:12]  # entries the rays actually touch
     flat = np.concatenate([flat, rng.choice(dF.size, 6, replace=False)])
