@@ -59,7 +59,13 @@ typedef enum {
 } dmv3d_status;
 
 typedef enum { DMV3D_F32 = 0, DMV3D_BF16 = 1 } dmv3d_dtype;
-typedef enum { DMV3D_AGG_MEAN = 0, DMV3D_AGG_SUM = 1 } dmv3d_agg;            /* A4 */
+/* A4; CONCAT (row f4) feeds [f_XY, f_XZ, f_YZ] (in_dim = 3 C) to the MLP */
+typedef enum { DMV3D_AGG_MEAN = 0, DMV3D_AGG_SUM = 1, DMV3D_AGG_CONCAT = 2 } dmv3d_agg;
+/* Texel addressing (A3).  ALIGN_CORNERS: texel centres at the box faces, clamped
+ * (grid_sample align_corners=True, border); HALFPIXEL_ZEROS (row f4): centres at
+ * (i + 1/2)/R of the box, corners outside the plane read as zero
+ * (grid_sample align_corners=False, padding zeros). */
+typedef enum { DMV3D_SAMPLE_ALIGN_CORNERS = 0, DMV3D_SAMPLE_HALFPIXEL_ZEROS = 1 } dmv3d_sample_mode;
 typedef enum { DMV3D_ACT_RELU = 0, DMV3D_ACT_SILU = 1, DMV3D_ACT_SOFTPLUS = 2 } dmv3d_act;
 typedef enum {
   DMV3D_ENGINE_AUTO = 0,   /* tensor cores when the shapes allow, else SIMT            */
@@ -82,10 +88,11 @@ typedef struct {
   dmv3d_dtype dtype;
   const void *data;      /* [3][R][R][C] DEVICE                                   */
   float aabb_min[3], aabb_max[3]; /* object box, default -1/+1    */
+  dmv3d_sample_mode sample_mode;  /* texel addressing, default ALIGN_CORNERS         */
 } dmv3d_triplane;
 
 /* Shared MLP decoder (reading A5-A7).  Layer l maps
- * in_l -> out_l with in_0 = in_dim (= channels), out_{L-1} = 4 (sigma, r, g, b),
+ * in_l -> out_l with in_0 = in_dim (= channels; 3 * channels for CONCAT), out_{L-1} = 4 (sigma, r, g, b),
  * every other width = hidden.  sigma = softplus(o_0 + density_shift);
  * c = sigmoid(o_{1..3}) * (1 + 2 eps) - eps. */
 typedef struct {
@@ -136,7 +143,7 @@ dmv3d_status dmv3d_timer_reset(dmv3d_timer *timer);
 dmv3d_status dmv3d_timer_read(dmv3d_timer *timer, double *total_ms, int64_t *launches);
 
 /* Scratch the TCGEN05 engine needs for this triplane/MLP (0 if it cannot run
- * them): 256 + 3*R*R*hidden*2 bytes. */
+ * them): 256 + (3*R*R + 1)*hidden*2 bytes (the extra row holds b0). */
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp);
 
 /* DDIM x0 -> x_{t-1} (readings A15-A20). */
@@ -247,13 +254,15 @@ dmv3d_status dmv3d_debug_ray_geometry(const dmv3d_cameras *cams, const float aab
                                       dmv3d_stream stream);
 /* Bit-exact sample set: t_k [n][N], point [n][N][3], texel [n][N][3][2]
  * (column, row index per plane), frac [n][N][3][2] (fractions); rays that
- * miss write zeros; `res` is the triplane resolution R.  Any output may be NULL. */
-dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const float aabb_min[3],
-                                       const float aabb_max[3], int32_t res,
+ * miss write zeros.  Only res, aabb and sample_mode of `grid` are read (its data
+ * may be NULL).  HALFPIXEL_ZEROS reports the unclamped lower texel index
+ * (-1 .. R-1) and its fraction.  Any output may be NULL. */
+dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const dmv3d_triplane *grid,
                                        const dmv3d_render_opts *opts,
                                        float *t_k, float *points, int32_t *texel, float *frac,
                                        dmv3d_stream stream);
-/* Aggregated triplane features at n points [n][3] -> feats [n][C] (fp32 math). */
+/* Aggregated triplane features at n points [n][3] -> feats [n][C] ([n][3C] for
+ * CONCAT) (fp32 math). */
 dmv3d_status dmv3d_debug_sample_features(const dmv3d_triplane *triplane, dmv3d_agg agg,
                                          int64_t n, const float *points, float *feats,
                                          dmv3d_stream stream);

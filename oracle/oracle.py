@@ -232,10 +232,11 @@ def grid_points(G, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
     return out
 
 
-def density_grid(tp, m, G, agg=AGG_MEAN, threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1)):
+def density_grid(tp, m, G, agg=AGG_MEAN, threads=0, aabb_min=(-1, -1, -1), aabb_max=(1, 1, 1),
+                 sample_mode=0):
     """sigma [G,G,G] and rgb [3,G,G,G] (fp64) on the density grid (row f3)."""
     keep = _Keep()
-    t = _triplane(tp, keep, aabb_min, aabb_max)
+    t = _triplane(tp, keep, aabb_min, aabb_max, sample_mode)
     mm = _mlp(m, keep)
     L = lib()
     L.orc_density_grid.argtypes = [ct.POINTER(_Triplane), ct.POINTER(_MLP), ct.c_int32, ct.c_int32,

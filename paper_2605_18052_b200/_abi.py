@@ -13,7 +13,8 @@ LIB_PATH = os.path.join(HERE, "libdmv3d.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_ALIGNMENT = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
-AGG_MEAN, AGG_SUM = 0, 1
+AGG_MEAN, AGG_SUM, AGG_CONCAT = 0, 1, 2
+SAMPLE_ALIGN_CORNERS, SAMPLE_HALFPIXEL_ZEROS = 0, 1
 ACT_RELU, ACT_SILU, ACT_SOFTPLUS = 0, 1, 2
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05 = 0, 1, 2
 
@@ -34,7 +35,8 @@ class Cameras(ct.Structure):
 
 class Triplane(ct.Structure):
     _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("dtype", ct.c_int32),
-                ("data", ct.c_void_p), ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3)]
+                ("data", ct.c_void_p), ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3),
+                ("sample_mode", ct.c_int32)]
 
 
 class MLP(ct.Structure):
@@ -97,8 +99,7 @@ def lib() -> ct.CDLL:
         L.dmv3d_debug_ray_geometry.argtypes = [P(Cameras), P(ct.c_float), P(ct.c_float),
                                                P(RenderOpts), ct.c_void_p, ct.c_void_p,
                                                ct.c_void_p, ct.c_void_p]
-        L.dmv3d_debug_sample_points.argtypes = [P(Cameras), P(ct.c_float), P(ct.c_float),
-                                                ct.c_int32, P(RenderOpts), ct.c_void_p,
+        L.dmv3d_debug_sample_points.argtypes = [P(Cameras), P(Triplane), P(RenderOpts), ct.c_void_p,
                                                 ct.c_void_p, ct.c_void_p, ct.c_void_p,
                                                 ct.c_void_p]
         L.dmv3d_debug_sample_features.argtypes = [P(Triplane), ct.c_int32, ct.c_int64,

@@ -17,7 +17,10 @@ from . import _abi
 _DT = {"f32": _abi.F32, "bf16": _abi.BF16}
 _TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16}
 _ENGINE = {"auto": _abi.ENGINE_AUTO, "simt": _abi.ENGINE_SIMT, "tcgen05": _abi.ENGINE_TCGEN05}
-_AGG = {"mean": _abi.AGG_MEAN, "sum": _abi.AGG_SUM}
+_AGG = {"mean": _abi.AGG_MEAN, "sum": _abi.AGG_SUM, "concat": _abi.AGG_CONCAT}
+# texel addressing (reading A3; row f4): grid_sample align_corners=True + border, or
+# align_corners=False + zero padding
+_SMODE = {"align_corners": _abi.SAMPLE_ALIGN_CORNERS, "halfpixel_zeros": _abi.SAMPLE_HALFPIXEL_ZEROS}
 
 
 def _ptr(t):
@@ -56,11 +59,13 @@ class DeviceMLP:
                         self.hidden_act, self.density_shift, self.rgb_widen_eps)
 
 
-def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0, 1.0, 1.0)):
+def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0, 1.0, 1.0),
+                    sample_mode="align_corners"):
     assert tp.dim() == 4 and tp.shape[0] == 3 and tp.shape[1] == tp.shape[2] and tp.is_contiguous()
     dt = {torch.float32: _abi.F32, torch.bfloat16: _abi.BF16}[tp.dtype]
     return _abi.Triplane(int(tp.shape[1]), int(tp.shape[3]), dt, tp.data_ptr(),
-                         (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max))
+                         (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max),
+                         _SMODE[sample_mode])
 
 
 def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, width: int):
@@ -91,7 +96,7 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
     dW = [torch.zeros(w.shape, device=dev, dtype=torch.float32) for w in mlp.weights]
     db = [torch.zeros(b.shape, device=dev, dtype=torch.float32) for b in mlp.biases]
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max)
+    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     o = opts_struct(**opts)
@@ -107,14 +112,15 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
 
 
 def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg="mean",
-                       aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None, engine="auto"):
+                       aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None, engine="auto",
+                       sample_mode="align_corners"):
     """sigma [G,G,G] (+ rgb [3,G,G,G]) of the decoder on the box grid."""
     G = int(grid_res)
     dev = triplane.device
     sigma = torch.empty((G, G, G), device=dev, dtype=torch.float32)
     rgb = torch.empty((3, G, G, G), device=dev, dtype=torch.float32) if want_rgb else None
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max)
+    t = triplane_struct(triplane, aabb_min, aabb_max, sample_mode)
     m = mlp.struct(keep)
     ws = workspace_for(t, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(agg=agg, engine=engine, workspace=ws, timer=timer)
@@ -206,7 +212,7 @@ def dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
     if alpha is None:
         alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max)
+    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     if "workspace" not in opts:
@@ -247,7 +253,7 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
     if alpha is None and want_alpha:
         alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
     keep = []
-    tt = triplane_struct(triplane, aabb_min, aabb_max)
+    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     if "workspace" not in opts:
@@ -286,7 +292,7 @@ def dmv3d_render_ddim_step_host(ws: Workspace, triplane, intrinsics, c2w, height
     """Host-buffer step: every tensor is a (pinned) CPU tensor; copies in/out are inside
     the library call, on `stream` (default: torch's current stream)."""
     keep = []
-    tt = triplane_struct(triplane)
+    tt = triplane_struct(triplane, sample_mode=opts.pop("sample_mode", "align_corners"))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     o = opts_struct(**opts)
@@ -318,7 +324,7 @@ def dmv3d_debug_ray_geometry(intrinsics, c2w, height, width, aabb_min=(-1.0,) * 
 
 def dmv3d_debug_sample_points(intrinsics, c2w, height, width, res, samples_per_ray,
                               aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, ray_range=None,
-                              jitter=False, seed=0):
+                              jitter=False, seed=0, sample_mode="align_corners"):
     V = int(c2w.shape[0])
     n = V * height * width if ray_range is None else ray_range[1] - ray_range[0]
     N = samples_per_ray
@@ -329,27 +335,29 @@ def dmv3d_debug_sample_points(intrinsics, c2w, height, width, res, samples_per_r
     frac = torch.empty((n, N, 3, 2), device=dev)
     c = cameras_struct(intrinsics, c2w, height, width)
     o = opts_struct(samples_per_ray=N, ray_range=ray_range, jitter=jitter, seed=seed)
-    lo, hi = (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max)
-    _abi.check(_abi.lib().dmv3d_debug_sample_points(ct.byref(c), lo, hi, res, ct.byref(o),
+    grid = _abi.Triplane(int(res), 4, _abi.F32, None, (ct.c_float * 3)(*aabb_min),
+                         (ct.c_float * 3)(*aabb_max), _SMODE[sample_mode])
+    _abi.check(_abi.lib().dmv3d_debug_sample_points(ct.byref(c), ct.byref(grid), ct.byref(o),
                                                     _ptr(t_k), _ptr(pts), _ptr(texel),
                                                     _ptr(frac), _stream(dev)))
     return t_k, pts, texel, frac
 
 
-def dmv3d_debug_sample_features(triplane, points, agg="mean"):
+def dmv3d_debug_sample_features(triplane, points, agg="mean", sample_mode="align_corners"):
     n = int(points.shape[0])
-    feats = torch.empty((n, int(triplane.shape[3])), device=triplane.device)
-    t = triplane_struct(triplane)
+    k = int(triplane.shape[3]) * (3 if agg == "concat" else 1)
+    feats = torch.empty((n, k), device=triplane.device)
+    t = triplane_struct(triplane, sample_mode=sample_mode)
     _abi.check(_abi.lib().dmv3d_debug_sample_features(ct.byref(t), _AGG[agg], n, _ptr(points),
                                                       _ptr(feats), _stream(triplane.device)))
     return feats
 
 
-def dmv3d_debug_decode(triplane, mlp: DeviceMLP, points, agg="mean"):
+def dmv3d_debug_decode(triplane, mlp: DeviceMLP, points, agg="mean", sample_mode="align_corners"):
     n = int(points.shape[0])
     out = torch.empty((n, 4), device=triplane.device)
     keep = []
-    t = triplane_struct(triplane)
+    t = triplane_struct(triplane, sample_mode=sample_mode)
     m = mlp.struct(keep)
     _abi.check(_abi.lib().dmv3d_debug_decode(ct.byref(t), ct.byref(m), _AGG[agg], n, _ptr(points),
                                              _ptr(out), _stream(triplane.device)))

@@ -86,6 +86,8 @@ dmv3d_status check_triplane(const dmv3d_triplane *t) {
   CHECK_ARG(t->dtype == DMV3D_F32 || t->dtype == DMV3D_BF16, "triplane: bad dtype");
   CHECK_ARG(t->data != nullptr, "triplane: data is NULL");
   CHECK_ALIGN(t->data, "triplane.data");
+  CHECK_ARG(t->sample_mode == DMV3D_SAMPLE_ALIGN_CORNERS || t->sample_mode == DMV3D_SAMPLE_HALFPIXEL_ZEROS,
+            "triplane: bad sample_mode");
   if (t->dtype == DMV3D_F32 && t->channels % 4)
     return fail(DMV3D_ERR_UNSUPPORTED, "triplane: fp32 needs channels % 4 == 0 (16-byte vectors)");
   if (t->dtype == DMV3D_BF16 && t->channels % 8)
@@ -93,10 +95,18 @@ dmv3d_status check_triplane(const dmv3d_triplane *t) {
   return check_aabb(t->aabb_min, t->aabb_max);
 }
 
-dmv3d_status check_mlp(const dmv3d_mlp *m, const dmv3d_triplane *t) {
+dmv3d_status check_agg(int agg) {
+  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM || agg == DMV3D_AGG_CONCAT, "bad agg");
+  return DMV3D_OK;
+}
+
+dmv3d_status check_mlp(const dmv3d_mlp *m, const dmv3d_triplane *t, int agg) {
   CHECK_ARG(m != nullptr, "mlp is NULL");
   CHECK_ARG(m->num_layers >= 2 && m->num_layers <= kMaxLayers, "mlp: num_layers must be in [2, 8]");
-  CHECK_ARG(m->in_dim == t->channels, "mlp: in_dim must equal triplane channels (mean/sum aggregation)");
+  if (agg == DMV3D_AGG_CONCAT)
+    CHECK_ARG(m->in_dim == 3 * t->channels, "mlp: in_dim must be 3 * channels (concat aggregation)");
+  else
+    CHECK_ARG(m->in_dim == t->channels, "mlp: in_dim must equal triplane channels (mean/sum aggregation)");
   CHECK_ARG(m->hidden >= 1, "mlp: hidden must be >= 1");
   CHECK_ARG(m->dtype == DMV3D_F32 || m->dtype == DMV3D_BF16, "mlp: bad dtype");
   CHECK_ARG(m->hidden_act >= DMV3D_ACT_RELU && m->hidden_act <= DMV3D_ACT_SOFTPLUS, "mlp: bad hidden_act");
@@ -113,7 +123,8 @@ dmv3d_status check_mlp(const dmv3d_mlp *m, const dmv3d_triplane *t) {
 dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
   CHECK_ARG(o != nullptr, "opts is NULL");
   CHECK_ARG(o->samples_per_ray >= 1 && o->samples_per_ray <= 1024, "opts: samples_per_ray must be in [1, 1024]");
-  CHECK_ARG(o->agg == DMV3D_AGG_MEAN || o->agg == DMV3D_AGG_SUM, "opts: bad agg");
+  CHECK_ARG(o->agg == DMV3D_AGG_MEAN || o->agg == DMV3D_AGG_SUM || o->agg == DMV3D_AGG_CONCAT,
+            "opts: bad agg");
   CHECK_ARG(o->term_eps >= 0.0f && o->term_eps < 1.0f, "opts: term_eps must be in [0, 1)");
   CHECK_ARG(o->engine >= DMV3D_ENGINE_AUTO && o->engine <= DMV3D_ENGINE_TCGEN05, "opts: bad engine");
   for (int c = 0; c < 3; ++c) CHECK_ARG(isfinite(o->bg_rgb[c]), "opts: non-finite bg");
@@ -137,6 +148,7 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
   P.R = t->res;
   P.C = t->channels;
   P.tp = t->data;
+  P.smode = t->sample_mode;
   for (int a = 0; a < 3; ++a) {
     P.lo[a] = t->aabb_min[a];
     P.hi[a] = t->aabb_max[a];
@@ -213,12 +225,12 @@ dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3
                          Engine &e) {
   const bool bf16 = t->dtype == DMV3D_BF16 && m->dtype == DMV3D_BF16;
   const bool tc_ok = bf16 && m->hidden_act == DMV3D_ACT_RELU &&
-                     tc_supported(m->in_dim, m->hidden, m->num_layers);
+                     tc_supported(t->channels, m->hidden, m->num_layers);
   const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden);
   if (o->engine == DMV3D_ENGINE_TCGEN05) {
     if (!tc_ok)
       return fail(DMV3D_ERR_UNSUPPORTED,
-                  "engine TCGEN05 needs bf16 triplane + weights, ReLU, hidden 64, in_dim % 8 == 0 "
+                  "engine TCGEN05 needs bf16 triplane + weights, ReLU, hidden 64, channels % 8 == 0 "
                   "(<= 256), 2 <= L <= 8");
     if (!ws_ok)
       return fail(DMV3D_ERR_INVALID_ARG,
@@ -230,7 +242,7 @@ dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3
     e = Engine::TC;
     return DMV3D_OK;
   }
-  if (!simt_supported(m->in_dim, m->hidden))
+  if (!simt_supported(m->in_dim, m->hidden, o->agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "SIMT engine: unsupported (in_dim, hidden) = (" +
                                            std::to_string(m->in_dim) + ", " + std::to_string(m->hidden) + ")");
   e = Engine::SIMT;
@@ -249,9 +261,9 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
   dmv3d_status s;
   if ((s = check_cams(c)) != DMV3D_OK) return s;
   if ((s = check_triplane(t)) != DMV3D_OK) return s;
-  if ((s = check_mlp(m, t)) != DMV3D_OK) return s;
   const int64_t nrays = (int64_t)c->num_views * c->height * c->width;
   if ((s = check_opts(o, nrays)) != DMV3D_OK) return s;
+  if ((s = check_mlp(m, t, o->agg)) != DMV3D_OK) return s;
   if (rgb) CHECK_ALIGN(rgb, "rgb");
   if (alpha) CHECK_ALIGN(alpha, "alpha");
   RenderParams P;
@@ -301,7 +313,7 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
 extern "C" {
 
 const char *dmv3d_last_error(void) { return g_err.c_str(); }
-const char *dmv3d_version(void) { return "dmv3d-b200 0.2 (sm_100a)"; }
+const char *dmv3d_version(void) { return "dmv3d-b200 0.3 (sm_100a)"; }
 
 dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_opts *opts,
                                 float *out, dmv3d_stream stream) {
@@ -341,16 +353,16 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
   dmv3d_status s;
   if ((s = check_cams(cams)) != DMV3D_OK) return s;
   if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
-  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
   if ((s = check_opts(opts, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
     return s;
+  if ((s = check_mlp(mlp, triplane, opts->agg)) != DMV3D_OK) return s;
   CHECK_ARG(grad_rgb && grad_triplane && grad_weights && grad_biases, "backward: NULL gradient buffer");
   CHECK_ALIGN(grad_rgb, "grad_rgb");
   if (grad_alpha) CHECK_ALIGN(grad_alpha, "grad_alpha");
   CHECK_ALIGN(grad_triplane, "grad_triplane");
   if (mlp->hidden_act != DMV3D_ACT_RELU)
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: ReLU hidden layers only");
-  if (!backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers))
+  if (!backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers, opts->agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: unsupported (in_dim, hidden, L)");
   RenderParams P;
   fill_common(P, triplane, cams, mlp, opts);
@@ -375,7 +387,6 @@ dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp 
   g_err.clear();
   dmv3d_status s;
   if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
-  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
   dmv3d_render_opts o{};
   o.samples_per_ray = 1;
   o.ray_begin = o.ray_end = -1;
@@ -387,7 +398,8 @@ dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp 
     o.workspace_bytes = opts->workspace_bytes;
     o.timer = opts->timer;
   }
-  CHECK_ARG(o.agg == DMV3D_AGG_MEAN || o.agg == DMV3D_AGG_SUM, "bad agg");
+  if ((s = check_agg(o.agg)) != DMV3D_OK) return s;
+  if ((s = check_mlp(mlp, triplane, o.agg)) != DMV3D_OK) return s;
   CHECK_ARG(o.engine >= DMV3D_ENGINE_AUTO && o.engine <= DMV3D_ENGINE_TCGEN05, "bad engine");
   CHECK_ARG(grid_res >= 2 && grid_res <= 2048, "density grid: grid_res must be in [2, 2048]");
   CHECK_ARG(sigma != nullptr, "density grid: sigma is NULL");
@@ -408,7 +420,7 @@ dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp 
     return cuda_status(launch_render_tc(P, reinterpret_cast<cudaStream_t>(stream)),
                        "density grid launch");
   }
-  if (!simt_supported(mlp->in_dim, mlp->hidden))
+  if (!simt_supported(mlp->in_dim, mlp->hidden, o.agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "density grid: unsupported (in_dim, hidden)");
   return cuda_status(launch_density_grid(P, triplane->dtype == DMV3D_BF16,
                                          mlp->dtype == DMV3D_BF16, grid_res, sigma, rgb,
@@ -460,7 +472,7 @@ dmv3d_status dmv3d_timer_read(dmv3d_timer *t, double *total_ms, int64_t *launche
 
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp) {
   if (!triplane || !mlp || triplane->res < 2) return 0;
-  if (!tc_supported(mlp->in_dim, mlp->hidden, mlp->num_layers)) return 0;
+  if (!tc_supported(triplane->channels, mlp->hidden, mlp->num_layers)) return 0;
   return tc_workspace_bytes(triplane->res, mlp->hidden);
 }
 
@@ -527,25 +539,23 @@ dmv3d_status dmv3d_debug_ray_geometry(const dmv3d_cameras *cams, const float aab
                      "ray geometry launch");
 }
 
-dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const float aabb_min[3],
-                                       const float aabb_max[3], int32_t res,
+dmv3d_status dmv3d_debug_sample_points(const dmv3d_cameras *cams, const dmv3d_triplane *grid,
                                        const dmv3d_render_opts *opts, float *t_k, float *points,
                                        int32_t *texel, float *frac, dmv3d_stream stream) {
   g_err.clear();
   dmv3d_status s;
   if ((s = check_cams(cams)) != DMV3D_OK) return s;
-  CHECK_ARG(aabb_min && aabb_max, "aabb is NULL");
-  CHECK_ARG(res >= 2, "res must be >= 2");
-  if ((s = check_aabb(aabb_min, aabb_max)) != DMV3D_OK) return s;
+  CHECK_ARG(grid != nullptr, "grid is NULL");
+  CHECK_ARG(grid->res >= 2, "res must be >= 2");
+  CHECK_ARG(grid->sample_mode == DMV3D_SAMPLE_ALIGN_CORNERS ||
+                grid->sample_mode == DMV3D_SAMPLE_HALFPIXEL_ZEROS,
+            "bad sample_mode");
+  if ((s = check_aabb(grid->aabb_min, grid->aabb_max)) != DMV3D_OK) return s;
   if ((s = check_opts(opts, (int64_t)cams->num_views * cams->height * cams->width)) != DMV3D_OK)
     return s;
-  dmv3d_triplane t{};
-  t.res = res;
+  dmv3d_triplane t = *grid;
   t.channels = 4;
-  for (int a = 0; a < 3; ++a) {
-    t.aabb_min[a] = aabb_min[a];
-    t.aabb_max[a] = aabb_max[a];
-  }
+  t.data = nullptr;
   RenderParams P;
   fill_common(P, &t, cams, nullptr, opts);
   return cuda_status(launch_sample_points(P, t_k, points, texel, frac,
@@ -565,7 +575,7 @@ dmv3d_status dmv3d_debug_sample_features(const dmv3d_triplane *triplane, dmv3d_a
   g_err.clear();
   dmv3d_status s;
   if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
-  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  if ((s = check_agg(agg)) != DMV3D_OK) return s;
   CHECK_ARG(n >= 0, "n must be >= 0");
   CHECK_ARG(n == 0 || (points && feats), "points / feats is NULL");
   if (n) {
@@ -589,15 +599,15 @@ dmv3d_status dmv3d_debug_decode(const dmv3d_triplane *triplane, const dmv3d_mlp 
   g_err.clear();
   dmv3d_status s;
   if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
-  if ((s = check_mlp(mlp, triplane)) != DMV3D_OK) return s;
-  CHECK_ARG(agg == DMV3D_AGG_MEAN || agg == DMV3D_AGG_SUM, "bad agg");
+  if ((s = check_agg(agg)) != DMV3D_OK) return s;
+  if ((s = check_mlp(mlp, triplane, agg)) != DMV3D_OK) return s;
   CHECK_ARG(n >= 0, "n must be >= 0");
   CHECK_ARG(n == 0 || (points && sigma_rgb), "points / sigma_rgb is NULL");
   if (n) {
     CHECK_ALIGN(points, "points");
     CHECK_ALIGN(sigma_rgb, "sigma_rgb");
   }
-  if (!simt_supported(mlp->in_dim, mlp->hidden))
+  if (!simt_supported(mlp->in_dim, mlp->hidden, agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "decode: unsupported (in_dim, hidden)");
   const dmv3d_cameras c = no_cams();
   RenderParams P;

@@ -53,7 +53,7 @@ __device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const M
   }
 }
 
-template <bool BF16, int K, int HD>
+template <bool BF16, int K, int HD, bool CAT>
 __global__ void __launch_bounds__(kBwThreads, 1)
     render_backward_kernel(const __grid_constant__ RenderParams P,
                            const __grid_constant__ GradParams Gp, int w_bf16) {
@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(kBwThreads, 1)
   float *dst = dstage + wib * 32 * HD;               // [32][HD]
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const float scale = P.agg == 0 ? (1.0f / 3.0f) : 1.0f;
+  const float scale = (!CAT && P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
+  constexpr int CP = CAT ? K / 3 : K;  // channels per plane
   const int64_t HWp = (int64_t)P.H * P.W;
 
   for (int64_t r = P.ray_begin + warp0; r < P.ray_end; r += nwarps) {
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         float p[3];
         sample_p(ray, sample_t(ray, delta, k, u), p);
         float x[K];
-        gather_features<BF16, K>(P, p, x);
+        gather_features<BF16, K, CAT>(P, p, x);
         mlp_decode<K, HD>(P, m, x, col, kBwThreads, sigma, c);
       }
       const float tau = valid ? sigma * delta : 0.0f;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
         sample_p(ray, sample_t(ray, delta, k, u), p);
         float x[K];
-        gather_features<BF16, K>(P, p, x);
+        gather_features<BF16, K, CAT>(P, p, x);
 #pragma unroll
         for (int c = 0; c < K; ++c) col[c * kBwThreads] = x[c];
         mlp_forward_store<K, HD>(P, m, col, kBwThreads, o4);
@@ -227,16 +228,16 @@ __global__ void __launch_bounds__(kBwThreads, 1)
           // dL/dh0 -> the 12 bilinear corners of the three planes
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
-            const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext);
-            const float gx = 1.0f - cell.fx, gy = 1.0f - cell.fy;
-            const float wc[4] = {gx * gy * scale, cell.fx * gy * scale, gx * cell.fy * scale,
-                                 cell.fx * cell.fy * scale};
+            const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext, P.smode);
+            const float wc[4] = {cell.wx0 * cell.wy0 * scale, cell.wx1 * cell.wy0 * scale,
+                                 cell.wx0 * cell.wy1 * scale, cell.wx1 * cell.wy1 * scale};
             const int64_t rowC = (int64_t)P.R * P.C;
             const int64_t off[4] = {cell.off, cell.off + P.C, cell.off + rowC, cell.off + rowC + P.C};
-            for (int cc = 0; cc < K; ++cc) {
+            const int x0 = CAT ? pl * CP : 0;  // this plane's columns of W0
+            for (int cc = 0; cc < CP; ++cc) {
               float dh = 0.0f;
 #pragma unroll
-              for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + cc] * d[q];
+              for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + x0 + cc] * d[q];
 #pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (wc[e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wc[e] * dh);
@@ -274,16 +275,19 @@ size_t backward_smem_bytes(int K, int HD, int L) {
 }
 
 #define DMV3D_BW_SHAPES(X) \
-  X(4, 16)                 \
-  X(8, 16)                 \
-  X(16, 32)                \
-  X(32, 64)                \
-  X(80, 64)
+  X(4, 16, false)          \
+  X(8, 16, false)          \
+  X(16, 32, false)         \
+  X(32, 64, false)         \
+  X(80, 64, false)         \
+  X(12, 16, true)          \
+  X(24, 16, true)          \
+  X(48, 32, true)
 
-bool backward_supported(int K, int HD, int L) {
+bool backward_supported(int K, int HD, int L, bool concat) {
   if (backward_smem_bytes(K, HD, L) > 232448) return false;
-#define X(k, h) \
-  if (K == k && HD == h) return true;
+#define X(k, h, cat) \
+  if (K == k && HD == h && concat == cat) return true;
   DMV3D_BW_SHAPES(X)
 #undef X
   return false;
@@ -294,10 +298,10 @@ cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, 
   const int64_t rays = P.ray_end - P.ray_begin;
   if (rays <= 0) return cudaSuccess;
   const size_t smem = backward_smem_bytes(P.K, P.HD, P.L);
-#define X(k, h)                                                                                  \
-  if (P.K == k && P.HD == h)                                                                     \
-    return tp_bf16 ? bw_launch(render_backward_kernel<true, k, h>, smem, rays, st, P, Gp, w_bf16) \
-                   : bw_launch(render_backward_kernel<false, k, h>, smem, rays, st, P, Gp, w_bf16);
+#define X(k, h, cat)                                                                                  \
+  if (P.K == k && P.HD == h && (P.agg == 2) == cat)                                                   \
+    return tp_bf16 ? bw_launch(render_backward_kernel<true, k, h, cat>, smem, rays, st, P, Gp, w_bf16) \
+                   : bw_launch(render_backward_kernel<false, k, h, cat>, smem, rays, st, P, Gp, w_bf16);
   DMV3D_BW_SHAPES(X)
 #undef X
   return cudaErrorInvalidValue;

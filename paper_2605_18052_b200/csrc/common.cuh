@@ -27,6 +27,7 @@ struct RenderParams {
   const void *tp;  // [3][R][R][C]
   float lo[3], hi[3];
   float inv_ext[3];  // 1/(hi-lo) if a power of two, else 0 (see texel_coord)
+  int32_t smode;     // texel addressing: 0 align-corners/clamp, 1 half-pixel/zeros (f4)
   // shared MLP
   int32_t L, K, HD;
   const void *w[kMaxLayers];
@@ -183,28 +184,70 @@ __device__ __forceinline__ void texel_coord(float q, float lo, float hi, float i
   f = __fsub_rn(px, __int2float_rn(ix));
 }
 
+// Row f4: half-pixel texel centres, (i + 1/2)/R of the box; the unclamped lower
+// index i0 = floor(s R - 1/2) lies in [-1, R-1] for points in the box.
+__device__ __forceinline__ void texel_coord_hp(float q, float lo, float hi, float inv, int R,
+                                               int &i0, float &f) {
+  const float num = __fsub_rn(q, lo);
+  const float s = (inv != 0.0f) ? __fmul_rn(num, inv) : __fdiv_rn(num, __fsub_rn(hi, lo));
+  const float px = __fsub_rn(__fmul_rn(s, __int2float_rn(R)), 0.5f);
+  const int ix = __float2int_rd(px);
+  i0 = ix;
+  f = __fsub_rn(px, __int2float_rn(ix));
+}
+
+// One axis of a bilinear cell in either addressing mode: the cell base i0 in
+// [0, R-2] and the weights of texels i0 and i0 + 1.  Half-pixel corners that
+// fall outside the plane get weight zero (zero padding), so every mode reads
+// the same in-range 2x2 cell.
+__device__ __forceinline__ void texel_axis(float q, float lo, float hi, float inv, int R,
+                                           int mode, int &i0, float &w0, float &w1) {
+  int ix;
+  float f;
+  if (mode == 0) {
+    texel_coord(q, lo, hi, inv, R, ix, f);
+    i0 = ix;
+    w0 = 1.0f - f;
+    w1 = f;
+    return;
+  }
+  texel_coord_hp(q, lo, hi, inv, R, ix, f);
+  const float g = 1.0f - f;
+  if (ix < 0) {  // only texel ix + 1 = 0 can be inside
+    i0 = 0;
+    w0 = ix == -1 ? f : 0.0f;
+    w1 = 0.0f;
+  } else if (ix > R - 2) {  // only texel ix = R - 1 can be inside
+    i0 = R - 2;
+    w0 = 0.0f;
+    w1 = ix == R - 1 ? g : 0.0f;
+  } else {
+    i0 = ix;
+    w0 = g;
+    w1 = f;
+  }
+}
+
 // Plane (a, b) for planes XY, XZ, YZ (reading A2).
 __device__ __forceinline__ int plane_axis_a(int pl) { return pl == 2 ? 1 : 0; }
 __device__ __forceinline__ int plane_axis_b(int pl) { return pl == 0 ? 1 : 2; }
 
-// One plane's bilinear cell: element offset of texel (iy, ix) and fractions.
+// One plane's bilinear cell: element offset of texel (iy, ix) and the per-axis
+// weights (corner (y, x) weighs wy[y] * wx[x]).
 struct Cell {
   int64_t off;  // element offset of corner (iy, ix) of plane pl
-  float fx, fy;
+  float wx0, wx1, wy0, wy1;
 };
 
 __device__ __forceinline__ Cell plane_cell(const float p[3], int pl, int R, int C,
                                            const float lo[3], const float hi[3],
-                                           const float inv[3]) {
+                                           const float inv[3], int mode) {
   const int a = plane_axis_a(pl), b = plane_axis_b(pl);
   int ix, iy;
-  float fx, fy;
-  texel_coord(p[a], lo[a], hi[a], inv[a], R, ix, fx);
-  texel_coord(p[b], lo[b], hi[b], inv[b], R, iy, fy);
   Cell c;
+  texel_axis(p[a], lo[a], hi[a], inv[a], R, mode, ix, c.wx0, c.wx1);
+  texel_axis(p[b], lo[b], hi[b], inv[b], R, mode, iy, c.wy0, c.wy1);
   c.off = (((int64_t)pl * R + iy) * R + ix) * C;
-  c.fx = fx;
-  c.fy = fy;
   return c;
 }
 

@@ -141,8 +141,13 @@ __global__ void sample_points_kernel(const __grid_constant__ RenderParams P, flo
 #pragma unroll
       for (int pl = 0; pl < 3; ++pl) {
         const int a = plane_axis_a(pl), b = plane_axis_b(pl);
-        texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], P.R, idx[2 * pl], fr[2 * pl]);
-        texel_coord(p[b], P.lo[b], P.hi[b], P.inv_ext[b], P.R, idx[2 * pl + 1], fr[2 * pl + 1]);
+        if (P.smode == 0) {
+          texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], P.R, idx[2 * pl], fr[2 * pl]);
+          texel_coord(p[b], P.lo[b], P.hi[b], P.inv_ext[b], P.R, idx[2 * pl + 1], fr[2 * pl + 1]);
+        } else {
+          texel_coord_hp(p[a], P.lo[a], P.hi[a], P.inv_ext[a], P.R, idx[2 * pl], fr[2 * pl]);
+          texel_coord_hp(p[b], P.lo[b], P.hi[b], P.inv_ext[b], P.R, idx[2 * pl + 1], fr[2 * pl + 1]);
+        }
       }
     }
     if (t_k) t_k[q] = t;

@@ -13,7 +13,7 @@ void timer_begin(void *timer, cudaStream_t st);
 void timer_end(void *timer, cudaStream_t st);
 
 // render_simt.cu
-bool simt_supported(int K, int HD);
+bool simt_supported(int K, int HD, bool concat);
 size_t simt_smem_bytes(int K, int HD, int L);
 cudaError_t launch_render_simt(const RenderParams &P, bool tp_bf16, bool w_bf16,
                                cudaStream_t st);
@@ -32,12 +32,12 @@ struct GradParams {
   float *dW[kMaxLayers];  // [out][in], accumulated
   float *db[kMaxLayers];  // [out], accumulated
 };
-bool backward_supported(int K, int HD, int L);
+bool backward_supported(int K, int HD, int L, bool concat);
 cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, bool tp_bf16,
                                    bool w_bf16, cudaStream_t st);
 
 // render_tc.cu (tcgen05 / TMEM engine)
-bool tc_supported(int K, int HD, int L);
+bool tc_supported(int C, int HD, int L);  // C = triplane channels per plane
 size_t tc_workspace_bytes(int R, int HD);
 cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
 

@@ -14,7 +14,7 @@
 namespace dmv3d {
 
 // ------------------------------------------------------ renderer kernel
-template <bool BF16, int K, int HD>
+template <bool BF16, int K, int HD, bool CAT>
 __global__ void __launch_bounds__(kSimtThreads)
     render_simt_kernel(const __grid_constant__ RenderParams P, int w_bf16) {
   extern __shared__ __align__(16) float smem[];
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kSimtThreads)
         float p[3];
         sample_p(ray, sample_t(ray, delta, k, u), p);
         float x[K];
-        gather_features<BF16, K>(P, p, x);
+        gather_features<BF16, K, CAT>(P, p, x);
         mlp_decode<K, HD>(P, m, x, my_act, blockDim.x, sigma, c);
       }
       // a5: front-to-back compositing as a warp prefix sum of optical depth
@@ -92,20 +92,20 @@ __global__ void __launch_bounds__(kSimtThreads)
 }
 
 // --------------------------------------------------------- debug kernels
-template <bool BF16, int K>
+template <bool BF16, int K, bool CAT>
 __global__ void features_kernel(const __grid_constant__ RenderParams P, int64_t n,
                                 const float *__restrict__ pts, float *__restrict__ out) {
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     const float p[3] = {pts[3 * q], pts[3 * q + 1], pts[3 * q + 2]};
     float x[K];
-    gather_features<BF16, K>(P, p, x);
+    gather_features<BF16, K, CAT>(P, p, x);
 #pragma unroll
     for (int c = 0; c < K; ++c) out[q * K + c] = x[c];
   }
 }
 
-template <bool BF16, int K, int HD>
+template <bool BF16, int K, int HD, bool CAT>
 __global__ void __launch_bounds__(kSimtThreads)
     decode_kernel(const __grid_constant__ RenderParams P, int w_bf16, int64_t n,
                   const float *__restrict__ pts, float *__restrict__ out) {
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kSimtThreads)
        q += (int64_t)gridDim.x * blockDim.x) {
     const float p[3] = {pts[3 * q], pts[3 * q + 1], pts[3 * q + 2]};
     float x[K];
-    gather_features<BF16, K>(P, p, x);
+    gather_features<BF16, K, CAT>(P, p, x);
     float sigma, c[3];
     mlp_decode<K, HD>(P, m, x, act + threadIdx.x, blockDim.x, sigma, c);
     out[4 * q] = sigma;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSimtThreads)
 
 // row f3: density grid for marching cubes: G^3 points on the box,
 // align-corners, x fastest; sigma [G^3] and optionally rgb [3][G^3]
-template <bool BF16, int K, int HD>
+template <bool BF16, int K, int HD, bool CAT>
 __global__ void __launch_bounds__(kSimtThreads)
     density_grid_kernel(const __grid_constant__ RenderParams P, int w_bf16, int G,
                         float *__restrict__ sigma, float *__restrict__ rgb) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kSimtThreads)
       p[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
     }
     float x[K];
-    gather_features<BF16, K>(P, p, x);
+    gather_features<BF16, K, CAT>(P, p, x);
     float sg, c[3];
     mlp_decode<K, HD>(P, m, x, act + threadIdx.x, blockDim.x, sg, c);
     sigma[q] = sg;
@@ -169,17 +169,22 @@ size_t simt_smem_bytes(int K, int HD, int L) {
   return floats * 4 + 16 + (size_t)HD * kSimtThreads * 4;
 }
 
+// (K, HD, CAT): K = MLP input width (3 C for the concat aggregation)
 #define DMV3D_SIMT_SHAPES(X) \
-  X(4, 16)                   \
-  X(8, 16)                   \
-  X(16, 32)                  \
-  X(32, 64)                  \
-  X(64, 64)                  \
-  X(80, 64)
+  X(4, 16, false)            \
+  X(8, 16, false)            \
+  X(16, 32, false)           \
+  X(32, 64, false)           \
+  X(64, 64, false)           \
+  X(80, 64, false)           \
+  X(12, 16, true)            \
+  X(24, 16, true)            \
+  X(48, 32, true)            \
+  X(96, 64, true)
 
-bool simt_supported(int K, int HD) {
-#define X(k, h) \
-  if (K == k && HD == h) return true;
+bool simt_supported(int K, int HD, bool concat) {
+#define X(k, h, cat) \
+  if (K == k && HD == h && concat == cat) return true;
   DMV3D_SIMT_SHAPES(X)
 #undef X
   return false;
@@ -208,9 +213,9 @@ cudaError_t launch_render_simt(const RenderParams &P, bool tp_bf16, bool w_bf16,
   const size_t smem = simt_smem_bytes(P.K, P.HD, P.L);
   const int64_t rays = P.ray_end - P.ray_begin;
   if (rays <= 0) return cudaSuccess;
-#define X(k, h)                                                                          \
-  if (P.K == k && P.HD == h) {                                                           \
-    auto fn = tp_bf16 ? render_simt_kernel<true, k, h> : render_simt_kernel<false, k, h>; \
+#define X(k, h, cat)                                                                     \
+  if (P.K == k && P.HD == h && (P.agg == 2) == cat) {                                    \
+    auto fn = tp_bf16 ? render_simt_kernel<true, k, h, cat> : render_simt_kernel<false, k, h, cat>; \
     int grid = 0;                                                                        \
     cudaError_t e = launch_cfg(fn, smem, rays, kSimtThreads, kSimtThreads / 32, st, grid); \
     if (e != cudaSuccess) return e;                                                      \
@@ -229,13 +234,14 @@ cudaError_t launch_features(const RenderParams &P, bool tp_bf16, int64_t n, cons
   if (n <= 0) return cudaSuccess;
   const int threads = 128;
   const int grid = (int)((n + threads - 1) / threads < 4096 ? (n + threads - 1) / threads : 4096);
-#define X(k, h)                                                               \
-  if (P.C == k) {                                                             \
-    auto fn = tp_bf16 ? features_kernel<true, k> : features_kernel<false, k>; \
-    fn<<<grid, threads, 0, st>>>(P, n, pts, out);                             \
-    return cudaGetLastError();                                                \
+#define X(k, cat)                                                                       \
+  if (P.C * (cat ? 3 : 1) == k && (P.agg == 2) == cat) {                                \
+    auto fn = tp_bf16 ? features_kernel<true, k, cat> : features_kernel<false, k, cat>; \
+    fn<<<grid, threads, 0, st>>>(P, n, pts, out);                                       \
+    return cudaGetLastError();                                                          \
   }
-  X(4, 0) X(8, 0) X(16, 0) X(32, 0) X(64, 0) X(80, 0)
+  X(4, false) X(8, false) X(16, false) X(32, false) X(64, false) X(80, false)
+  X(12, true) X(24, true) X(48, true) X(96, true)
 #undef X
   return cudaErrorInvalidValue;
 }
@@ -245,9 +251,9 @@ cudaError_t launch_density_grid(const RenderParams &P, bool tp_bf16, bool w_bf16
   const int64_t n = (int64_t)G * G * G;
   if (n <= 0) return cudaSuccess;
   const size_t smem = simt_smem_bytes(P.K, P.HD, P.L);
-#define X(k, h)                                                                             \
-  if (P.K == k && P.HD == h) {                                                              \
-    auto fn = tp_bf16 ? density_grid_kernel<true, k, h> : density_grid_kernel<false, k, h>; \
+#define X(k, h, cat)                                                                        \
+  if (P.K == k && P.HD == h && (P.agg == 2) == cat) {                                       \
+    auto fn = tp_bf16 ? density_grid_kernel<true, k, h, cat> : density_grid_kernel<false, k, h, cat>; \
     int grid = 0;                                                                           \
     cudaError_t e = launch_cfg(fn, smem, n, kSimtThreads, kSimtThreads, st, grid);          \
     if (e != cudaSuccess) return e;                                                         \
@@ -265,9 +271,9 @@ cudaError_t launch_decode(const RenderParams &P, bool tp_bf16, bool w_bf16, int6
                           const float *pts, float *out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = simt_smem_bytes(P.K, P.HD, P.L);
-#define X(k, h)                                                                         \
-  if (P.K == k && P.HD == h) {                                                          \
-    auto fn = tp_bf16 ? decode_kernel<true, k, h> : decode_kernel<false, k, h>;         \
+#define X(k, h, cat)                                                                    \
+  if (P.K == k && P.HD == h && (P.agg == 2) == cat) {                                   \
+    auto fn = tp_bf16 ? decode_kernel<true, k, h, cat> : decode_kernel<false, k, h, cat>; \
     int grid = 0;                                                                       \
     cudaError_t e = launch_cfg(fn, smem, n, kSimtThreads, kSimtThreads, st, grid);      \
     if (e != cudaSuccess) return e;                                                     \

@@ -52,10 +52,13 @@ constexpr uint32_t kWHidden = kTcHD * kWK * 2;         // 10 KiB per hidden laye
 constexpr uint32_t kWHead = 16 * kWK * 2;              // 2.5 KiB
 constexpr size_t kSmemLimit = 232448;                  // 227 KiB per CTA
 
-size_t tc_workspace_bytes(int R, int HD) { return kWsHeader + (size_t)3 * R * R * HD * 2; }
+// header (patch counter) + G [3 R R + 1][HD]: the last row holds b0 for the
+// half-pixel mode's bias column
+size_t tc_workspace_bytes(int R, int HD) { return kWsHeader + ((size_t)3 * R * R + 1) * HD * 2; }
 
-bool tc_supported(int K, int HD, int L) {
-  return HD == kTcHD && K >= 8 && K <= 256 && K % 8 == 0 && L >= 2 && L <= kMaxLayers;
+// C = channels per plane (the MLP input is 3 C for the concat aggregation)
+bool tc_supported(int C, int HD, int L) {
+  return HD == kTcHD && C >= 8 && C <= 256 && C % 8 == 0 && L >= 2 && L <= kMaxLayers;
 }
 
 template <int NG>
@@ -76,16 +79,22 @@ static size_t tc_smem_bytes(int L) {
 // ------------------------------------------------------------------ K0
 // G[t][o] = fp16(sum_c F[t][c] W0[o][c] + b0[o] * bscale); one warp per texel,
 // lane -> outputs (2 lane, 2 lane + 1); W0 transposed in smem (conflict-free).
+// W0 rows have stride `wstride` (3 C for the concat aggregation, whose planes are
+// projected by their own column block of W0).  Optionally zeroes the patch counter
+// and writes fp16(b0) to `gbias` (the bias row of the half-pixel mode).
 __global__ void __launch_bounds__(256)
-    preproject_kernel(const __nv_bfloat16 *__restrict__ F, int ntex, int C,
+    preproject_kernel(const __nv_bfloat16 *__restrict__ F, int ntex, int C, int wstride,
                       const __nv_bfloat16 *__restrict__ W0, const float *__restrict__ b0,
-                      float bscale, __half *__restrict__ G, unsigned int *counter) {
+                      float bscale, __half *__restrict__ G, unsigned int *counter,
+                      __half *__restrict__ gbias) {
   extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
   for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {
     const int o = e / C, c = e - o * C;
-    reinterpret_cast<float *>(swt)[c * kTcHD + o] = __bfloat162float(W0[e]);
+    reinterpret_cast<float *>(swt)[c * kTcHD + o] = __bfloat162float(W0[(size_t)o * wstride + c]);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && counter) *counter = 0u;
+  if (blockIdx.x == 0 && gbias && threadIdx.x < kTcHD)
+    gbias[threadIdx.x] = __float2half_rn(__ldg(b0 + threadIdx.x));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bias0 = __ldg(b0 + 2 * lane) * bscale, bias1 = __ldg(b0 + 2 * lane + 1) * bscale;
@@ -215,6 +224,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int slot = tid >> 3, q = tid & 7;
   const int R = P.R;
   const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
+  // half-pixel zero padding: the blend weights of a sample no longer sum to one per
+  // plane, so b0 is not folded into G but added by one extra A column (weight 1)
+  // that reads the bias row G[3 R R]
+  const int hb = P.smode != 0 ? 1 : 0;
 
   uint32_t mphase = 0;
   unsigned long long n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;
@@ -226,12 +239,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
     const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
     const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
     const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
-    const int ktot = base2 + ext1 * ext2;
+    const int ktex = base2 + ext1 * ext2;
+    const int ktot = ktex + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     if (tid < kpad) {
       const int kg = w0 + tid;
       int texel = -1;
-      if (kg < ktot) {
+      if (kg == ktex && hb) {
+        texel = 3 * R * R;
+      } else if (kg < ktex) {
         int loc, bw, ta0, tb0, pl;
         if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
         else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // SWIZZLE_128B (16-B chunk index XOR row index within each 1 KiB atom)
   auto stage = [&](const int *bb, int w0) {
     const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-    const int ktot = e0 * e1 + e0 * e2 + e1 * e2;
+    const int ktot = e0 * e1 + e0 * e2 + e1 * e2 + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     for (int e = tid; e < kpad * 8; e += 128) {
       const int kl = e >> 3, ch = e & 7;
@@ -308,7 +324,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     // the rays alive before c's compositing; rays that terminate in c get zero A
     // rows in c+1.
     int ix[3] = {0, 0, 0};
-    float fr[3] = {0.f, 0.f, 0.f};
+    float wl[3] = {0.f, 0.f, 0.f}, wh[3] = {0.f, 0.f, 0.f};  // weights of texels ix, ix + 1
     int par = 0;
     // geometry + window + staging of window 0 for the chunk starting at kk (the
     // chunk's bbox slot must still hold its reset state when this runs)
@@ -318,7 +334,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const int k = kk + q;
       const bool sv = spec_alive && (GRID || k < P.N);  // GRID: one point per row
       ix[0] = ix[1] = ix[2] = 0;
-      fr[0] = fr[1] = fr[2] = 0.f;
+      wl[0] = wl[1] = wl[2] = 0.f;
+      wh[0] = wh[1] = wh[2] = 0.f;
       if (sv) {
         float p[3];
         if constexpr (GRID) {
@@ -330,7 +347,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
           sample_p(ray, sample_t(ray, delta, k, u), p);
         }
 #pragma unroll
-        for (int a = 0; a < 3; ++a) texel_coord(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, ix[a], fr[a]);
+        for (int a = 0; a < 3; ++a)
+          texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
       }
       int mn[3], mx[3];
 #pragma unroll
@@ -363,11 +381,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
       // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); row-major bbox rows
       const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
-      const int ktot = base2 + ext1 * ext2;
+      const int ktex = base2 + ext1 * ext2;
+      const int ktot = ktex + hb;
       const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
       const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
       const int bws[3] = {ext0, ext0, ext1};
-      const float fa[3] = {fr[0], fr[0], fr[1]}, fb[3] = {fr[1], fr[2], fr[2]};
+      const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
+      const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
 
       // ---- blend on the tensor cores: window 0 was staged by prefetch; rare extra
       //      windows (> kTcKMax texels) are staged synchronously
@@ -378,14 +398,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
         if (sv) {
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
-            const float gx = 1.0f - fa[pl], gy = (1.0f - fb[pl]) * wscale, fy = fb[pl] * wscale;
+            const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
             const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
-            const float w4[4] = {gx * gy, fa[pl] * gy, gx * fy, fa[pl] * fy};
+            const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
             const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
           }
+          if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
+            ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);  // fp16 1.0: + b0
         }
         if (w0 > 0) {  // synchronous staging of an extra window
           fill_table(bb, w0);
@@ -544,19 +566,29 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // K0: G = F W0^T + b0 (fp16), zero the patch counter
+  // K0: G = F W0^T + b0 * bscale (fp16), zero the patch counter.  The bias is split
+  // over the three planes except for the mean, whose A weights carry the 1/3; the
+  // half-pixel mode adds it through the bias row instead.
   const int ntex = 3 * P.R * P.R;
   const size_t s0 = (size_t)kTcHD * P.C * 4;
   cudaError_t e = cudaFuncSetAttribute(preproject_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
   if (e != cudaSuccess) return e;
-  int g0 = (ntex * 32 + 255) / 256;
+  const float bscale = P.smode != 0 ? 0.0f : (P.agg == 0 ? 1.0f : (1.0f / 3.0f));
+  const __nv_bfloat16 *F = reinterpret_cast<const __nv_bfloat16 *>(P.tp);
+  const __nv_bfloat16 *W0 = reinterpret_cast<const __nv_bfloat16 *>(P.w[0]);
+  const bool cat = P.agg == 2;
+  const int nlaunch = cat ? 3 : 1, nt = cat ? P.R * P.R : ntex;
+  int g0 = (nt * 32 + 255) / 256;
   if (g0 > sms * 8) g0 = sms * 8;
-  preproject_kernel<<<g0, 256, s0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(P.tp), ntex, P.C,
-                                         reinterpret_cast<const __nv_bfloat16 *>(P.w[0]), P.b[0],
-                                         P.agg == 0 ? 1.0f : (1.0f / 3.0f), G, counter);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  for (int pl = 0; pl < nlaunch; ++pl) {
+    preproject_kernel<<<g0, 256, s0, st>>>(F + (size_t)pl * nt * P.C, nt, P.C, cat ? 3 * P.C : P.C,
+                                           W0 + (size_t)pl * P.C, P.b[0], bscale,
+                                           G + (size_t)pl * nt * kTcHD, pl == 0 ? counter : nullptr,
+                                           pl == 0 ? G + (size_t)ntex * kTcHD : nullptr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
   const bool ng4 = tc_smem_bytes<4>(P.L) <= kSmemLimit;

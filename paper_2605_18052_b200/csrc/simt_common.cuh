@@ -8,16 +8,20 @@
 namespace dmv3d {
 
 // ------------------------------------------------------------ a3: gather
-template <bool BF16, int K>
+// K = MLP input width; CAT (concat aggregation, row f4): K = 3 C and plane pl
+// fills x[pl C, (pl + 1) C), else K = C and the planes are summed (x 1/3: mean).
+template <bool BF16, int K, bool CAT = false>
 __device__ __forceinline__ void gather_features(const RenderParams &P, const float p[3],
                                                 float x[K]) {
+  constexpr int CP = CAT ? K / 3 : K;
 #pragma unroll
   for (int c = 0; c < K; ++c) x[c] = 0.0f;
 #pragma unroll
   for (int pl = 0; pl < 3; ++pl) {
-    const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext);
-    const float gx = 1.0f - cell.fx, gy = 1.0f - cell.fy;
-    const float w00 = gx * gy, w01 = cell.fx * gy, w10 = gx * cell.fy, w11 = cell.fx * cell.fy;
+    const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext, P.smode);
+    const float w00 = cell.wx0 * cell.wy0, w01 = cell.wx1 * cell.wy0, w10 = cell.wx0 * cell.wy1,
+                w11 = cell.wx1 * cell.wy1;
+    float *xp = x + (CAT ? pl * CP : 0);
     const int64_t rowC = (int64_t)P.R * P.C;
     if constexpr (BF16) {
       const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(P.tp) + cell.off;
@@ -26,15 +30,15 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
       const uint4 *t10 = reinterpret_cast<const uint4 *>(base + rowC);
       const uint4 *t11 = reinterpret_cast<const uint4 *>(base + rowC + P.C);
 #pragma unroll
-      for (int q = 0; q < K / 8; ++q) {
+      for (int q = 0; q < CP / 8; ++q) {
         const uint4 a = __ldg(t00 + q), b = __ldg(t01 + q), c = __ldg(t10 + q), d = __ldg(t11 + q);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
         const uint32_t cv[4] = {c.x, c.y, c.z, c.w}, dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          x[8 * q + 2 * e] += w00 * bf16lo(av[e]) + w01 * bf16lo(bv[e]) + w10 * bf16lo(cv[e]) +
+          xp[8 * q + 2 * e] += w00 * bf16lo(av[e]) + w01 * bf16lo(bv[e]) + w10 * bf16lo(cv[e]) +
                               w11 * bf16lo(dv[e]);
-          x[8 * q + 2 * e + 1] += w00 * bf16hi(av[e]) + w01 * bf16hi(bv[e]) +
+          xp[8 * q + 2 * e + 1] += w00 * bf16hi(av[e]) + w01 * bf16hi(bv[e]) +
                                   w10 * bf16hi(cv[e]) + w11 * bf16hi(dv[e]);
         }
       }
@@ -45,16 +49,16 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
       const float4 *t10 = reinterpret_cast<const float4 *>(base + rowC);
       const float4 *t11 = reinterpret_cast<const float4 *>(base + rowC + P.C);
 #pragma unroll
-      for (int q = 0; q < K / 4; ++q) {
+      for (int q = 0; q < CP / 4; ++q) {
         const float4 a = __ldg(t00 + q), b = __ldg(t01 + q), c = __ldg(t10 + q), d = __ldg(t11 + q);
-        x[4 * q + 0] += w00 * a.x + w01 * b.x + w10 * c.x + w11 * d.x;
-        x[4 * q + 1] += w00 * a.y + w01 * b.y + w10 * c.y + w11 * d.y;
-        x[4 * q + 2] += w00 * a.z + w01 * b.z + w10 * c.z + w11 * d.z;
-        x[4 * q + 3] += w00 * a.w + w01 * b.w + w10 * c.w + w11 * d.w;
+        xp[4 * q + 0] += w00 * a.x + w01 * b.x + w10 * c.x + w11 * d.x;
+        xp[4 * q + 1] += w00 * a.y + w01 * b.y + w10 * c.y + w11 * d.y;
+        xp[4 * q + 2] += w00 * a.z + w01 * b.z + w10 * c.z + w11 * d.z;
+        xp[4 * q + 3] += w00 * a.w + w01 * b.w + w10 * c.w + w11 * d.w;
       }
     }
   }
-  if (P.agg == 0) {
+  if (!CAT && P.agg == 0) {
 #pragma unroll
     for (int c = 0; c < K; ++c) x[c] *= (1.0f / 3.0f);
   }

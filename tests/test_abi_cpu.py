@@ -71,6 +71,11 @@ def _valid_structs(keep):
     (lambda t, c, m, o: setattr(c, "c2w", c.c2w + 8), _abi.ERR_ALIGNMENT),
     (lambda t, c, m, o: setattr(o, "engine", _abi.ENGINE_TCGEN05), _abi.ERR_UNSUPPORTED),
     (lambda t, c, m, o: setattr(m, "hidden", 17), _abi.ERR_UNSUPPORTED),
+    (lambda t, c, m, o: setattr(t, "sample_mode", 2), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(o, "agg", 3), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(o, "agg", _abi.AGG_CONCAT), _abi.ERR_INVALID_ARG),  # in_dim != 3C
+    (lambda t, c, m, o: (setattr(o, "agg", _abi.AGG_CONCAT), setattr(m, "in_dim", 24),
+                         setattr(m, "hidden", 32)), _abi.ERR_UNSUPPORTED),  # no (24, 32) concat kernel
 ])
 def test_render_argument_validation(mutate, status):
     keep = []
@@ -120,3 +125,30 @@ def test_product_schedule_matches_oracle():
     ts = schedule.ddim_timesteps()
     assert ts[0] == 980 and ts[-1] == 0 and len(ts) == 50
     assert schedule.ddim_pairs()[-1] == (0, -1)
+
+
+def test_struct_layout_matches_header(tmp_path):
+    """The ctypes mirrors in _abi have the size and field offsets the C compiler gives
+    the structs of include/dmv3d.h (gcc, host ABI)."""
+    structs = {"dmv3d_cameras": _abi.Cameras, "dmv3d_triplane": _abi.Triplane,
+               "dmv3d_mlp": _abi.MLP, "dmv3d_render_opts": _abi.RenderOpts,
+               "dmv3d_ddim_params": _abi.DdimParams}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "dmv3d.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f in py._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    r = os.system(f"gcc -I{os.path.join(ROOT, 'include')} {src} -o {exe}")
+    assert r == 0
+    got = {}
+    for ln in os.popen(str(exe)).read().splitlines():
+        name, field, val = ln.split()
+        got[(name, field)] = int(val)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ct.sizeof(py), cname
+        for f in py._fields_:
+            assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
