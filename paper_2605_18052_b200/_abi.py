@@ -9,7 +9,8 @@ import ctypes as ct
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdmv3d.so")
+# DMV3D_LIB selects an instrumented in-tree build (tools/phases.py); default: the product
+LIB_PATH = os.environ.get("DMV3D_LIB") or os.path.join(HERE, "libdmv3d.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_ALIGNMENT = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1

@@ -36,6 +36,25 @@
 
 namespace dmv3d {
 
+// Phase timing (tools/phases.py builds the library with -DDMV3D_PHASES): every thread
+// accumulates clock64 deltas per phase; each group's row 0 adds them to counters[8..15].
+#ifdef DMV3D_PHASES
+#define PH_DECL                                            \
+  unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
+  long long ph_t = clock64();
+#define PH(i)                         \
+  do {                                \
+    const long long ph_n = clock64(); \
+    ph_acc[i] += ph_n - ph_t;         \
+    ph_t = ph_n;                      \
+  } while (0)
+#else
+#define PH_DECL
+#define PH(i) \
+  do {        \
+  } while (0)
+#endif
+
 constexpr int kTcHD = 64;       // hidden width of the tensor-core engine
 constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
@@ -231,6 +250,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
   uint32_t mphase = 0;
   unsigned long long n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;
+  PH_DECL
   int chunk_ctr = 0;
 
   // column -> texel table of the tile's window [w0, w0 + kpad) (one column per thread);
@@ -279,6 +299,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     ptx::bar_sync(bar_id, 128);
     const int64_t patch = sh->patch[g];
     if (patch >= npatch) break;
+    PH(7);
     int v = 0, i = 0, j = 0;
     int64_t r = 0;
     bool pix;
@@ -373,6 +394,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
     bool have = ptx::bar_red_or(bar_id, 128, alive);
     if (have) prefetch(0, alive);
+    PH(0);
     for (int k0 = 0; have;) {
       const int k = k0 + q;
       const bool sv = alive && (GRID || k < P.N);
@@ -414,6 +436,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
           ptx::bar_sync(bar_id, 128);
           stage(bb, w0);
         }
+        PH(1);
         ptx::cp_async_wait_all();
         ptx::fence_proxy_async_smem();
         ptx::bar_sync(bar_id, 128);
@@ -430,16 +453,19 @@ __global__ void __launch_bounds__(128 * NG, 1)
         mphase ^= 1u;
       }
       ptx::tc_fence_after();
+      PH(2);
 
       // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
       const int k1 = k0 + kChunk;
       const bool nxt = !GRID && k1 < P.N;
       if (nxt) prefetch(k1, alive);
+      PH(3);
 
       // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
       //      (A operand from TMEM), weights in shared memory
       for (int l = 1; l < L; ++l) {
         act_epilogue(tmem_row, tmem_row + kTcHD);
+        PH(4);
         ptx::tc_fence_before();
         ptx::bar_sync(bar_id, 128);
         if (tid == 0) {
@@ -456,6 +482,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
         ptx::tc_fence_after();
+        PH(5);
       }
       // ---- head: sigma, rgb (a4)
       uint32_t o4[4];
@@ -506,6 +533,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       k0 = k1;
       have = nxt && ptx::bar_red_or(bar_id, 128, alive);
+      PH(6);
     }
     ptx::cp_async_wait_all();  // a prefetch for a chunk nobody needs may still be landing
     // ---- ray epilogue: reduce the 8 lanes, write rgb/alpha (+ DDIM x_{t-1})
@@ -518,6 +546,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
     if (!GRID && pix && q < 3) ray_epilogue(P, v, i, j, q, q == 0 ? acc0 : (q == 1 ? acc1 : acc2), T);
   }
 
+#ifdef DMV3D_PHASES
+  if (P.counters && tid == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(P.counters + 8 + i, ph_acc[i]);
+#endif
   if (P.counters) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {

@@ -61,10 +61,10 @@ int main() {
   cudaMalloc(&d, 8);
   const int smem = 128 * 128 * 2 + 256 * 128 * 2 + 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int layout : {0, 2})
-    for (int n : {64, 256})
-      for (int chains : {1, 2})
-        for (int ks : {1, 4, 8}) {
+  for (int layout : {0})
+    for (int n : {16, 64, 128, 256})
+      for (int chains : {1, 2, 4, 8})
+        for (int ks : {1, 8}) {
           if (chains * n > 512) continue;
           k<<<1, 128, smem>>>(2000, ks, n, layout, chains, d);
           cudaError_t e = cudaDeviceSynchronize();
