@@ -63,13 +63,14 @@ __global__ void __launch_bounds__(kBwThreads, 1)
   scratch = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(scratch) + 15) & ~uintptr_t(15));
   const int L = P.L;
   const int rows = K + (L - 1) * HD;
-  float *dstage = scratch + rows * kBwThreads;  // [warps][32 samples][HD]
+  constexpr int kDs = HD + 4;  // padded delta row: a lane's LDS.128 hits distinct banks
+  float *dstage = scratch + rows * kBwThreads;  // [warps][32 samples][kDs]
   __syncthreads();
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float *col = scratch + threadIdx.x;               // this lane's column (stride 128)
   float *wcol = scratch + wib * 32;                  // the warp's 32 columns
-  float *dst = dstage + wib * 32 * HD;               // [32][HD]
+  float *dst = dstage + wib * 32 * kDs;              // [32][kDs]
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float scale = (!CAT && P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
@@ -175,31 +176,31 @@ __global__ void __launch_bounds__(kBwThreads, 1)
       float dtau = gA * TN;
 #pragma unroll
       for (int q = 0; q < 3; ++q) dtau += g[q] * (Tk1 * c[q] - R[q]);
-      float d[HD];
-#pragma unroll
-      for (int q = 0; q < HD; ++q) d[q] = 0.0f;
-      if (valid) {
-        d[0] = dtau * delta * sigmoid_f(z0);
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          d[1 + q] = g[q] * w * (1.0f + 2.0f * P.weps) * sg[q] * (1.0f - sg[q]);
+      // ---- the head's delta (dL/d o, o = sigma / rgb pre-activations) -> this lane's
+      //      staged row; all deltas live in shared memory (no per-thread arrays)
+      float *myd = dst + lane * kDs;
+      {
+        float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+          const float cs = w * (1.0f + 2.0f * P.weps);
+          d4 = make_float4(dtau * delta * sigmoid_f(z0), g[0] * cs * sg[0] * (1.0f - sg[0]),
+                           g[1] * cs * sg[1] * (1.0f - sg[1]), g[2] * cs * sg[2] * (1.0f - sg[2]));
+        }
+        *reinterpret_cast<float4 *>(myd) = d4;
       }
       // ---- back through the MLP, layer L-1 .. 0
       for (int l = L - 1; l >= 0; --l) {
         const int in = l == 0 ? K : HD;
         const int out = l == L - 1 ? 4 : HD;
         const int hrow = l == 0 ? 0 : K + (l - 1) * HD;
-        // stage this lane's delta; lanes then own output rows q for the outer product
-#pragma unroll
-        for (int q = 0; q < HD; ++q)
-          if (q < out) dst[lane * HD + q] = d[q];
-        __syncwarp();
+        __syncwarp();  // every lane's delta row is staged
+        // dW_l += d (x) h_l, db_l += d: lanes own output rows q, summing the warp's 32 samples
         for (int q = lane; q < out; q += 32) {
           float dq[32];
           float bsum = 0.0f;
 #pragma unroll
           for (int s = 0; s < 32; ++s) {
-            dq[s] = dst[s * HD + q];
+            dq[s] = dst[s * kDs + q];
             bsum += dq[s];
           }
           if (bsum != 0.0f) atomicAdd(Gp.db[l] + q, bsum);
@@ -211,21 +212,48 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             if (sum != 0.0f) atomicAdd(Gp.dW[l] + (size_t)q * in + ii, sum);
           }
         }
-        __syncwarp();
-        if (l > 0) {
-          // dh = W_l^T d; ReLU mask from h_l > 0; the new delta overwrites h_l in place
-          for (int ii = 0; ii < in; ++ii) {
-            float dh = 0.0f;
+        __syncwarp();  // h_l is consumed: it may be overwritten by dh
+        // dh = W_l^T d (lane = sample), 16 inputs at a time: 4-wide broadcast weight loads
+        // against the lane's own delta row; ReLU-masked by h_l > 0 for l > 0, written over h_l
+        const float *W = m.W[l];
+        for (int i0 = 0; i0 < in; i0 += 16) {
+          float acc[16];
 #pragma unroll
-            for (int q = 0; q < HD; ++q)
-              if (q < out) dh += m.W[l][q * in + ii] * d[q];
-            const float h = col[(hrow + ii) * kBwThreads];
-            col[(hrow + ii) * kBwThreads] = h > 0.0f ? dh : 0.0f;
+          for (int t = 0; t < 16; ++t) acc[t] = 0.0f;
+          for (int q = 0; q < out; q += 4) {
+            const float4 d4 = *reinterpret_cast<const float4 *>(myd + q);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float *wr = W + (q + j) * in + i0;
+#pragma unroll
+              for (int t = 0; t < 16; t += 4) {
+                if (i0 + t < in) {
+                  const float4 w4 = *reinterpret_cast<const float4 *>(wr + t);
+                  acc[t] += w4.x * dv[j];
+                  acc[t + 1] += w4.y * dv[j];
+                  acc[t + 2] += w4.z * dv[j];
+                  acc[t + 3] += w4.w * dv[j];
+                }
+              }
+            }
           }
 #pragma unroll
-          for (int q = 0; q < HD; ++q) d[q] = col[(hrow + q) * kBwThreads];
+          for (int t = 0; t < 16; ++t) {
+            if (i0 + t < in) {
+              float *c = col + (hrow + i0 + t) * kBwThreads;
+              *c = (l == 0 || *c > 0.0f) ? acc[t] : 0.0f;
+            }
+          }
+        }
+        if (l > 0) {
+          // the next delta (layer l-1's outputs) = the masked dh just written
+          for (int q = 0; q < HD; q += 4)
+            *reinterpret_cast<float4 *>(myd + q) =
+                make_float4(col[(hrow + q) * kBwThreads], col[(hrow + q + 1) * kBwThreads],
+                            col[(hrow + q + 2) * kBwThreads], col[(hrow + q + 3) * kBwThreads]);
         } else if (valid) {
-          // dL/dh0 -> the 12 bilinear corners of the three planes
+          // dL/dh0 (rows [0, K) of this lane's column) -> the 12 bilinear corners
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
             const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext, P.smode);
@@ -233,19 +261,17 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                                  cell.wx0 * cell.wy1 * scale, cell.wx1 * cell.wy1 * scale};
             const int64_t rowC = (int64_t)P.R * P.C;
             const int64_t off[4] = {cell.off, cell.off + P.C, cell.off + rowC, cell.off + rowC + P.C};
-            const int x0 = CAT ? pl * CP : 0;  // this plane's columns of W0
+            const int x0 = CAT ? pl * CP : 0;  // this plane's columns of h0
             for (int cc = 0; cc < CP; ++cc) {
-              float dh = 0.0f;
-#pragma unroll
-              for (int q = 0; q < HD; ++q) dh += m.W[0][q * K + x0 + cc] * d[q];
+              const float dh = col[(x0 + cc) * kBwThreads];
 #pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (wc[e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wc[e] * dh);
             }
           }
         }
-        __syncwarp();
       }
+      __syncwarp();
       Tc *= expf(-__shfl_sync(0xffffffffu, S, 31));
 #pragma unroll
       for (int q = 0; q < 3; ++q) Pc[q] += tot[q];
@@ -271,7 +297,7 @@ static cudaError_t bw_launch(Fn fn, size_t smem, int64_t rays, cudaStream_t st, 
 
 size_t backward_smem_bytes(int K, int HD, int L) {
   const size_t mlp = (size_t)HD * K + (size_t)(L - 2) * HD * HD + 4 * HD + (size_t)(L - 1) * HD + 4;
-  return (mlp + 4 + (size_t)(K + (L - 1) * HD) * kBwThreads + (size_t)4 * 32 * HD) * 4;
+  return (mlp + 4 + (size_t)(K + (L - 1) * HD) * kBwThreads + (size_t)4 * 32 * (HD + 4)) * 4;
 }
 
 #define DMV3D_BW_SHAPES(X) \
