@@ -23,7 +23,7 @@ namespace dmv3d {
 constexpr int kBwThreads = 128;
 
 template <int K, int HD>
-__device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const MlpSmem &m,
+__device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const MlpSmem<K, HD> &m,
                                                   float *col, int stride, float o4[4]) {
   // col rows: [0, K) = h0, [K + (l-1) HD, K + l HD) = h_l (l >= 1, post-ReLU)
   const int L = P.L;
@@ -32,8 +32,8 @@ __device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const M
     const float *hin = col + (l == 0 ? 0 : (K + (l - 1) * HD)) * stride;
     float *hout = col + (K + l * HD) * stride;
     for (int o = 0; o < HD; ++o) {
-      const float *wr = m.W[l] + o * in;
-      float acc = m.B[l][o];
+      const float *wr = m.W(l) + o * in;
+      float acc = m.B(l)[o];
       for (int i = 0; i < in; i += 4) {
         const float4 w4 = *reinterpret_cast<const float4 *>(wr + i);
         acc += w4.x * hin[i * stride] + w4.y * hin[(i + 1) * stride] + w4.z * hin[(i + 2) * stride] +
@@ -46,8 +46,8 @@ __device__ __forceinline__ void mlp_forward_store(const RenderParams &P, const M
   const int in = L == 1 ? K : HD;
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
-    const float *wr = m.W[L - 1] + o * in;
-    float acc = m.B[L - 1][o];
+    const float *wr = m.W(L - 1) + o * in;
+    float acc = m.B(L - 1)[o];
     for (int i = 0; i < in; ++i) acc += wr[i] * h[i * stride];
     o4[o] = acc;
   }
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     render_backward_kernel(const __grid_constant__ RenderParams P,
                            const __grid_constant__ GradParams Gp, int w_bf16) {
   extern __shared__ __align__(16) float smem[];
-  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  const MlpSmem<K, HD> m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
   float *scratch = smem + mlp_smem_floats<K, HD>(P.L);
   scratch = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(scratch) + 15) & ~uintptr_t(15));
   const int L = P.L;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         __syncwarp();  // h_l is consumed: it may be overwritten by dh
         // dh = W_l^T d (lane = sample), 16 inputs at a time: 4-wide broadcast weight loads
         // against the lane's own delta row; ReLU-masked by h_l > 0 for l > 0, written over h_l
-        const float *W = m.W[l];
+        const float *W = m.W(l);
         for (int i0 = 0; i0 < in; i0 += 16) {
           float acc[16];
 #pragma unroll

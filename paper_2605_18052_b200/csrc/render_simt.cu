@@ -18,7 +18,7 @@ template <bool BF16, int K, int HD, bool CAT>
 __global__ void __launch_bounds__(kSimtThreads)
     render_simt_kernel(const __grid_constant__ RenderParams P, int w_bf16) {
   extern __shared__ __align__(16) float smem[];
-  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  const MlpSmem<K, HD> m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
   float *act = smem + mlp_smem_floats<K, HD>(P.L);
   act = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(act) + 15) & ~uintptr_t(15));
   __syncthreads();
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kSimtThreads)
     decode_kernel(const __grid_constant__ RenderParams P, int w_bf16, int64_t n,
                   const float *__restrict__ pts, float *__restrict__ out) {
   extern __shared__ __align__(16) float smem[];
-  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  const MlpSmem<K, HD> m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
   float *act = smem + mlp_smem_floats<K, HD>(P.L);
   act = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(act) + 15) & ~uintptr_t(15));
   __syncthreads();
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kSimtThreads)
     density_grid_kernel(const __grid_constant__ RenderParams P, int w_bf16, int G,
                         float *__restrict__ sigma, float *__restrict__ rgb) {
   extern __shared__ __align__(16) float smem[];
-  const MlpSmem m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
+  const MlpSmem<K, HD> m = setup_mlp<K, HD>(P, smem, w_bf16 != 0);
   float *act = smem + mlp_smem_floats<K, HD>(P.L);
   act = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(act) + 15) & ~uintptr_t(15));
   __syncthreads();

@@ -67,9 +67,18 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
 // ------------------------------------------------------------ a4: MLP
 // Shared-memory layout (fp32): W0 [HD][K], W_l [HD][HD] (l = 1..L-2),
 // W_{L-1} [4][HD], then biases b0 [HD], b_l [HD], b_{L-1} [4].
+// Pointers are computed, not stored in an indexed array: a runtime layer index into a
+// pointer array would place the struct in local memory (one LDL per weight-row access).
+template <int K, int HD>
 struct MlpSmem {
-  const float *W[kMaxLayers];
-  const float *B[kMaxLayers];
+  float *base;
+  int L;
+  __device__ __forceinline__ float *W(int l) const {
+    return base + (l == 0 ? 0 : K * HD + (l - 1) * HD * HD);
+  }
+  __device__ __forceinline__ float *B(int l) const {
+    return base + K * HD + (L - 2) * HD * HD + 4 * HD + l * HD;
+  }
 };
 
 template <int K, int HD>
@@ -78,12 +87,12 @@ __device__ __forceinline__ int mlp_smem_floats(int L) {
 }
 
 template <int K, int HD>
-__device__ __forceinline__ void fill_weights(const RenderParams &P, const MlpSmem &m,
+__device__ __forceinline__ void fill_weights(const RenderParams &P, const MlpSmem<K, HD> &m,
                                              bool w_bf16) {
   for (int l = 0; l < P.L; ++l) {
     const int in = l == 0 ? K : HD;
     const int out = l == P.L - 1 ? 4 : HD;
-    float *dst = const_cast<float *>(m.W[l]);
+    float *dst = m.W(l);
     const int n = in * out;
     if (w_bf16) {
       const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(P.w[l]);
@@ -98,15 +107,15 @@ __device__ __forceinline__ void fill_weights(const RenderParams &P, const MlpSme
 // h0 [K] in registers -> (sigma, rgb).  `act` is this thread's column of a
 // [HD][blockDim] fp32 scratch (stride blockDim), conflict-free.
 template <int K, int HD>
-__device__ __forceinline__ void mlp_decode(const RenderParams &P, const MlpSmem &m,
+__device__ __forceinline__ void mlp_decode(const RenderParams &P, const MlpSmem<K, HD> &m,
                                            const float x[K], float *act, int stride,
                                            float &sigma, float rgb[3]) {
   const int L = P.L;
   // layer 0
   if (L > 1) {
     for (int o = 0; o < HD; ++o) {
-      const float *wr = m.W[0] + o * K;
-      float acc = m.B[0][o];
+      const float *wr = m.W(0) + o * K;
+      float acc = m.B(0)[o];
 #pragma unroll
       for (int i = 0; i < K; i += 4) {
         const float4 w4 = *reinterpret_cast<const float4 *>(wr + i);
@@ -121,8 +130,8 @@ __device__ __forceinline__ void mlp_decode(const RenderParams &P, const MlpSmem 
 #pragma unroll
     for (int i = 0; i < HD; ++i) h[i] = act[i * stride];
     for (int o = 0; o < HD; ++o) {
-      const float *wr = m.W[l] + o * HD;
-      float acc = m.B[l][o];
+      const float *wr = m.W(l) + o * HD;
+      float acc = m.B(l)[o];
 #pragma unroll
       for (int i = 0; i < HD; i += 4) {
         const float4 w4 = *reinterpret_cast<const float4 *>(wr + i);
@@ -138,8 +147,8 @@ __device__ __forceinline__ void mlp_decode(const RenderParams &P, const MlpSmem 
   float o4[4];
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
-    const float *wr = m.W[L - 1] + o * HD;
-    float acc = m.B[L - 1][o];
+    const float *wr = m.W(L - 1) + o * HD;
+    float acc = m.B(L - 1)[o];
 #pragma unroll
     for (int i = 0; i < HD; i += 4) {
       const float4 w4 = *reinterpret_cast<const float4 *>(wr + i);
@@ -153,20 +162,14 @@ __device__ __forceinline__ void mlp_decode(const RenderParams &P, const MlpSmem 
 }
 
 template <int K, int HD>
-__device__ __forceinline__ MlpSmem setup_mlp(const RenderParams &P, float *smem, bool w_bf16) {
-  MlpSmem m;
-  float *cur = smem;
-  for (int l = 0; l < P.L; ++l) {
-    const int in = l == 0 ? K : HD;
-    const int out = l == P.L - 1 ? 4 : HD;
-    m.W[l] = cur;
-    cur += in * out;
-  }
+__device__ __forceinline__ MlpSmem<K, HD> setup_mlp(const RenderParams &P, float *smem, bool w_bf16) {
+  MlpSmem<K, HD> m;
+  m.base = smem;
+  m.L = P.L;
   for (int l = 0; l < P.L; ++l) {
     const int out = l == P.L - 1 ? 4 : HD;
-    m.B[l] = cur;
-    for (int e = threadIdx.x; e < out; e += blockDim.x) cur[e] = __ldg(P.b[l] + e);
-    cur += out;
+    float *b = m.B(l);
+    for (int e = threadIdx.x; e < out; e += blockDim.x) b[e] = __ldg(P.b[l] + e);
   }
   fill_weights<K, HD>(P, m, w_bf16);
   return m;

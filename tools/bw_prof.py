@@ -6,9 +6,9 @@ w = wl.make_workload("cfg2")
 dev = torch.device("cuda", 0)
 tp = torch.from_numpy(w.triplane).to(dev).to(torch.bfloat16).contiguous()
 m = api.DeviceMLP.from_host(wl.bf16_mlp(w.mlp), "bf16", dev)
-cams = wl.concat_cameras(wl.input_cameras(128, 128, 4), wl.novel_cameras(128, 128, 4))
+cams = wl.input_cameras(128, 128, 2)
 intr = torch.from_numpy(cams.intrinsics).to(dev); c2w = torch.from_numpy(cams.c2w).to(dev)
-g = torch.randn((8, 3, 128, 128), device=dev); gA = torch.randn((8, 128, 128), device=dev)
+g = torch.randn((2, 3, 128, 128), device=dev); gA = torch.randn((2, 128, 128), device=dev)
 for _ in range(2):
     api.dmv3d_render_backward(tp, intr, c2w, 128, 128, m, g, gA, samples_per_ray=128)
 torch.cuda.synchronize()
