@@ -252,21 +252,73 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             *reinterpret_cast<float4 *>(myd + q) =
                 make_float4(col[(hrow + q) * kBwThreads], col[(hrow + q + 1) * kBwThreads],
                             col[(hrow + q + 2) * kBwThreads], col[(hrow + q + 3) * kBwThreads]);
-        } else if (valid) {
-          // dL/dh0 (rows [0, K) of this lane's column) -> the 12 bilinear corners
+        } else {
+          // dL/dh0 (rows [0, K) of this lane's column) -> the 12 bilinear corners of the
+          // three planes, x the aggregation scale
+          const int64_t rowC = (int64_t)P.R * P.C;
+          float wcs[3][4];
+          int64_t offs[3];
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
             const Cell cell = plane_cell(p, pl, P.R, P.C, P.lo, P.hi, P.inv_ext, P.smode);
-            const float wc[4] = {cell.wx0 * cell.wy0 * scale, cell.wx1 * cell.wy0 * scale,
-                                 cell.wx0 * cell.wy1 * scale, cell.wx1 * cell.wy1 * scale};
-            const int64_t rowC = (int64_t)P.R * P.C;
-            const int64_t off[4] = {cell.off, cell.off + P.C, cell.off + rowC, cell.off + rowC + P.C};
-            const int x0 = CAT ? pl * CP : 0;  // this plane's columns of h0
-            for (int cc = 0; cc < CP; ++cc) {
-              const float dh = col[(x0 + cc) * kBwThreads];
+            const float sc = valid ? scale : 0.0f;
+            wcs[pl][0] = cell.wx0 * cell.wy0 * sc;
+            wcs[pl][1] = cell.wx1 * cell.wy0 * sc;
+            wcs[pl][2] = cell.wx0 * cell.wy1 * sc;
+            wcs[pl][3] = cell.wx1 * cell.wy1 * sc;
+            offs[pl] = cell.off;
+          }
+          constexpr int NCH = (K + 31) / 32;
+          if (32 * NCH <= (L - 1) * HD) {
+            // Lanes switch from samples to channels, so each RED covers 32 consecutive
+            // channels of one texel instead of 32 scattered texels: dh0 goes through a
+            // skewed sample-major scratch in the warp's dead hidden-activation rows, each
+            // sample's cells and corner weights through its (dead) delta row.
+            uint32_t *cr = reinterpret_cast<uint32_t *>(myd);
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (wc[e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wc[e] * dh);
+            for (int pl = 0; pl < 3; ++pl) {
+              cr[pl * 6] = (uint32_t)((uint64_t)offs[pl] & 0xffffffffu);
+              cr[pl * 6 + 1] = (uint32_t)((uint64_t)offs[pl] >> 32);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cr[pl * 6 + 2 + e] = __float_as_uint(wcs[pl][e]);
+            }
+            float *tsc = wcol + K * kBwThreads;
+            for (int c = 0; c < K; ++c)
+              tsc[(lane * NCH + (c >> 5)) * kBwThreads + ((c + lane) & 31)] = valid ? col[c * kBwThreads] : 0.0f;
+            __syncwarp();
+            for (int s2 = 0; s2 < 32; ++s2) {
+              const uint32_t *cs = reinterpret_cast<const uint32_t *>(dst + s2 * kDs);
+#pragma unroll
+              for (int pl = 0; pl < 3; ++pl) {
+                const float w0 = __uint_as_float(cs[pl * 6 + 2]), w1 = __uint_as_float(cs[pl * 6 + 3]);
+                const float w2 = __uint_as_float(cs[pl * 6 + 4]), w3 = __uint_as_float(cs[pl * 6 + 5]);
+                if (w0 == 0.0f && w1 == 0.0f && w2 == 0.0f && w3 == 0.0f) continue;  // warp-uniform
+                const int64_t off = (int64_t)(((uint64_t)cs[pl * 6 + 1] << 32) | cs[pl * 6]);
+                const int x0 = CAT ? pl * CP : 0;
+                for (int k0 = 0; k0 < CP; k0 += 32) {
+                  const int cc = k0 + lane;
+                  if (cc < CP) {
+                    const int c = x0 + cc;
+                    const float v = tsc[(s2 * NCH + (c >> 5)) * kBwThreads + ((c + s2) & 31)];
+                    if (w0 != 0.0f) atomicAdd(Gp.dF + off + cc, w0 * v);
+                    if (w1 != 0.0f) atomicAdd(Gp.dF + off + P.C + cc, w1 * v);
+                    if (w2 != 0.0f) atomicAdd(Gp.dF + off + rowC + cc, w2 * v);
+                    if (w3 != 0.0f) atomicAdd(Gp.dF + off + rowC + P.C + cc, w3 * v);
+                  }
+                }
+              }
+            }
+          } else if (valid) {
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+              const int64_t off[4] = {offs[pl], offs[pl] + P.C, offs[pl] + rowC, offs[pl] + rowC + P.C};
+              const int x0 = CAT ? pl * CP : 0;  // this plane's columns of h0
+              for (int cc = 0; cc < CP; ++cc) {
+                const float dh = col[(x0 + cc) * kBwThreads];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (wcs[pl][e] != 0.0f) atomicAdd(Gp.dF + off[e] + cc, wcs[pl][e] * dh);
+              }
             }
           }
         }
