@@ -8,7 +8,7 @@
 #include "../paper_2605_18052_b200/csrc/tc_ptx.cuh"
 using namespace dmv3d;
 
-__global__ void k(int iters, int ksteps, int n, int ts, long long *out) {
+__global__ void k(int iters, int ksteps, int n, int ts, int mm, long long *out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *A = sm, *B = sm + 128 * 128 * 2;
@@ -22,7 +22,7 @@ __global__ void k(int iters, int ksteps, int n, int ts, long long *out) {
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t idesc = ptx::idesc_f16(128, n, 0);
+  const uint32_t idesc = ptx::idesc_f16(mm, n, 0);
   const uint32_t d = tbase + (uint32_t)(g * (512 / G));  // group region (D then A for TS)
   uint32_t phase = 0;
   long long t0 = clock64();
@@ -57,17 +57,18 @@ int main() {
   cudaMalloc(&d, 8);
   const int smem = 128 * 128 * 2 + 256 * 128 * 2 + 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int ts : {0, 1})
-    for (int n : {16, 64, 128})
-      for (int G : {1, 4, 5, 8})
-        for (int ks : {1, 4, 8}) {
-          const int cols = n + (ts ? 8 * ks : 0);
-          if (G * cols > 512 || G * 128 > 1024) continue;
-          k<<<148, 128 * G, smem>>>(2000, ks, n, ts, d);
+  for (int mm : {128, 64})
+    for (int n : {64, 128, 256})
+      for (int G : {1, 2, 4})
+        for (int ks : {1, 8}) {
+          const int ts = 0;
+          if (G * n > 512) continue;
+          k<<<148, 128 * G, smem>>>(2000, ks, n, ts, mm, d);
           cudaError_t e = cudaDeviceSynchronize();
           cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-          printf("%s N=%3d groups=%d ksteps=%d : %5lld cycles/round  %.1f cycles/MMA per SM  (%s)\n",
-                 ts ? "TS" : "SS", n, G, ks, h, (double)h / (G * ks), cudaGetErrorString(e));
+          printf("SS M=%3d N=%3d groups=%d ksteps=%d : %5lld cycles/round  %.1f cycles/MMA per SM  (%s)\n",
+                 mm, n, G, ks, h, (double)h / (G * ks), cudaGetErrorString(e));
+          if (e != cudaSuccess) return 1;
         }
   return 0;
 }
