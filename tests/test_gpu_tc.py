@@ -173,3 +173,33 @@ def test_tc_all_miss_and_tiny():
     rgb, alpha, orgb, oalpha, _ = _tc_render(w)
     er, ea = _report(rgb, alpha, orgb, oalpha)
     assert er < RGB_TOL and ea < ALPHA_TOL
+
+
+@pytest.mark.parametrize("R,C,L,N", [(2, 8, 3, 5), (5, 256, 4, 24), (512, 8, 2, 40)])
+def test_tc_extreme_shapes(R, C, L, N):
+    """Smallest triplane (R = 2: one cell), the widest supported channel count (C = 256:
+    32 KiB of W0 in the pre-projection's shared memory), and R = 512 (texel windows far
+    beyond one 128-column MMA pass); odd N (partial chunks)."""
+    w = _wl(C=C, L=L, R=R, H=13, W=11, N=N, blob=False)
+    rgb, alpha, orgb, oalpha, _ = _tc_render(w, term_eps=0.0)
+    er, ea = _report(rgb, alpha, orgb, oalpha)
+    assert er < RGB_TOL and ea < ALPHA_TOL
+
+
+def test_tc_ray_range_shards_cover_the_image():
+    """Disjoint ray ranges (cut anywhere, including through 4x4 patches and views) write
+    exactly their pixels; together they equal the full render within the TC bar."""
+    w = _wl(C=32, L=4, H=14, W=18, N=32)
+    tp, intr, c2w, mlp = dev_workload(w)
+    H, W = 14, 18
+    V = w.cameras.num_views
+    full = api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, samples_per_ray=32, engine="tcgen05")
+    rgb = torch.full((V, 3, H, W), -7.0, device="cuda")
+    alpha = torch.full((V, H, W), -7.0, device="cuda")
+    cuts = [0, 37, 252, 253, 400, V * H * W]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, rgb=rgb, alpha=alpha, samples_per_ray=32,
+                               engine="tcgen05", ray_range=(a, b))
+    assert (alpha >= 0).all()  # every pixel written exactly by its shard
+    assert (rgb - full[0]).abs().max().item() < 1e-5
+    assert (alpha - full[1]).abs().max().item() < 1e-5
