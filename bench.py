@@ -34,10 +34,22 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "rays/s per denoise-step render (4 input + 4 novel views 256x256, fused DDIM)"
-WORKLOAD = ("cfg3: 4 input + 4 novel views 256x256, triplane 3x64x64x80 bf16, N=128 "
-            "midpoint samples/ray, shared MLP 80-64-64-64-4 (ReLU), fused DDIM on the 4 "
-            "input views along the 50-step grid 980..0, eta=0, term_eps=1e-4, white bg")
+# --config: cfg3 = BASELINE configs[2], the step north_star's target names ("a 4-view +
+# novel-view DDIM step at the paper's triplane and image sizes"): the default and the
+# headline.  cfg2 = configs[1] (4 input views at 128^2, paper-shaped triplane and MLP).
+CONFIGS = {
+    "cfg3": ("cfg3",
+             "rays/s per denoise-step render (4 input + 4 novel views 256x256, fused DDIM)",
+             "cfg3: 4 input + 4 novel views 256x256, triplane 3x64x64x80 bf16, N=128 "
+             "midpoint samples/ray, shared MLP 80-64-64-64-4 (ReLU), fused DDIM on the 4 "
+             "input views along the 50-step grid 980..0, eta=0, term_eps=1e-4, white bg"),
+    "cfg2": ("cfg2_bf16",
+             "rays/s per denoise-step render (4 input views 128x128, fused DDIM)",
+             "cfg2: 4 input views 128x128, triplane 3x64x64x80 bf16, N=128 midpoint "
+             "samples/ray, shared MLP 80-64-64-64-4 (ReLU), fused DDIM on the 4 views along "
+             "the 50-step grid 980..0, eta=0, term_eps=1e-4, white bg"),
+}
+METRIC, WORKLOAD = CONFIGS["cfg3"][1], CONFIGS["cfg3"][2]
 MLP_FLOPS_PER_SAMPLE = 2 * (80 * 64 + 2 * 64 * 64 + 64 * 4)  # 27,136
 TERM_EPS = 1e-4
 L2_FLUSH_BYTES = 256 << 20
@@ -130,7 +142,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2605_18052_b200 import workloads as wl
-    w = wl.make_workload("cfg3")
+    wname, metric, workload = CONFIGS[args.config]
+    w = wl.make_workload(wname)
     threads = os.cpu_count() or 1
     rays_per_step = 2048
     import oracle
@@ -144,14 +157,15 @@ def run_reference(args, rank, world):
             times.append(time.perf_counter() - t0)
     total = float(np.sum(times))
     value = rays_per_step * len(times) / total
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": "rays/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "rays_per_step_sampled": rays_per_step},
+            "config": {"workload": workload, "rays_per_step_sampled": rays_per_step},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{rays_per_step} random rays of cfg3 per step (of 524288), "
-                                       "full 128-sample march, fp64, no early termination"},
+                             "sample": f"{rays_per_step} random rays of {args.config} per step (of "
+                                       f"{w.num_rays}), full 128-sample march, fp64, no early "
+                                       "termination"},
             "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -164,6 +178,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS),
+                    help="cfg3 (default, BASELINE configs[2]) or cfg2 (configs[1])")
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -194,13 +210,15 @@ def main():
 
     # ---- inputs (one asset per rank, seeds 100 + rank), resident in HBM
     views_mode = args.mode == "views"
-    w = wl.make_workload("cfg3", asset=rank if (world > 1 and not views_mode) else None)
+    wname, metric, workload = CONFIGS[args.config]
+    w = wl.make_workload(wname, asset=rank if (world > 1 and not views_mode) else None)
     V, H, W = w.cameras.num_views, w.cameras.height, w.cameras.width
-    DV = w.ddim_views
-    tp = torch.from_numpy(w.triplane).to(dev).to(torch.bfloat16).contiguous()
+    DV = w.ddim_views or V  # the DDIM-updated (input) views
+    tdt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    tp = torch.from_numpy(w.triplane).to(dev).to(tdt).contiguous()
     intr = torch.from_numpy(w.cameras.intrinsics).to(dev)
     c2w = torch.from_numpy(w.cameras.c2w).to(dev)
-    mlp = api.DeviceMLP.from_host(w.mlp, "bf16", dev)
+    mlp = api.DeviceMLP.from_host(w.mlp, w.dtype, dev)
     ab = schedule.cosine_alpha_bar()
     pairs = schedule.ddim_pairs(50, 1000)
     x0 = torch.from_numpy(wl.gaussian((DV, 3, H, W), wl.SEED_XT)).to(dev)
@@ -266,11 +284,11 @@ def main():
     h_tp = tp.cpu().pin_memory()
     h_intr, h_c2w = intr.cpu().pin_memory(), c2w.cpu().pin_memory()
     h_mlp = api.DeviceMLP([x.cpu().pin_memory() for x in mlp.weights],
-                          [x.cpu().pin_memory() for x in mlp.biases], "bf16")
+                          [x.cpu().pin_memory() for x in mlp.biases], w.dtype)
     h_x = [x0.cpu().pin_memory(), torch.empty(x0.shape).pin_memory()]
     h_rgb = torch.empty(rgb.shape).pin_memory()
     h_alpha = torch.empty(alpha.shape).pin_memory()
-    h2d = (h_tp.numel() * 2 + h_intr.numel() * 4 + h_c2w.numel() * 4 + h_x[0].numel() * 4
+    h2d = (h_tp.numel() * h_tp.element_size() + h_intr.numel() * 4 + h_c2w.numel() * 4 + h_x[0].numel() * 4
            + sum(x.numel() * x.element_size() for x in h_mlp.weights + h_mlp.biases))
     d2h = h_x[0].numel() * 4 + h_rgb.numel() * 4 + h_alpha.numel() * 4
 
@@ -338,15 +356,15 @@ def main():
         threads = os.cpu_count() or 1
         r_rate, n_rays, secs = oracle_rate(w, args.cpu_budget, threads)
         cpu = {"value": r_rate, "unit": "rays/s", "cores": threads, "kind": "oracle",
-               "sample": f"{n_rays} random rays of cfg3 (of {rays}) in {secs:.1f} s; full "
+               "sample": f"{n_rays} random rays of {args.config} (of {rays}) in {secs:.1f} s; full "
                          f"128-sample march, fp64, no early termination"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
+        line = {"metric": metric, "value": value, "unit": "rays/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong" if views_mode else "weak",
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-                "config": {"workload": WORKLOAD,
+                "config": {"workload": workload,
                            "rays_per_step": units_per_step, "assets": 1 if views_mode else world,
                            "engine": engine_used,
                            "l2": "flushed between timed steps (256 MiB write); triplane re-read "
