@@ -183,10 +183,12 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--mode", default="assets", choices=["assets", "views"],
+    ap.add_argument("--mode", default="assets", choices=["assets", "views", "views-p2p"],
                     help="assets: one asset per rank, no data-path collective (weak scaling, "
                          "default); views: one asset's views split across ranks with an NCCL "
-                         "triplane broadcast + all-gather per step (strong scaling)")
+                         "triplane broadcast + all-gather per step (strong scaling); views-p2p: "
+                         "the same split, outputs assembled by the render kernel's NVLink peer "
+                         "stores into symmetric memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -209,7 +211,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs (one asset per rank, seeds 100 + rank), resident in HBM
-    views_mode = args.mode == "views"
+    views_mode = args.mode in ("views", "views-p2p")
     wname, metric, workload = CONFIGS[args.config]
     w = wl.make_workload(wname, asset=rank if (world > 1 and not views_mode) else None)
     V, H, W = w.cameras.num_views, w.cameras.height, w.cameras.width
@@ -238,7 +240,8 @@ def main():
             from paper_2605_18052_b200 import dist as pdist
             xp, _, _ = pdist.denoise_step_view_sharded(
                 tp, intr, c2w, H, W, mlp, ab, t, tp_, x_in, DV, samples_per_ray=w.samples_per_ray,
-                term_eps=TERM_EPS, engine=args.engine, counters=cnt, timer=timer)
+                term_eps=TERM_EPS, engine=args.engine, counters=cnt, timer=timer,
+                p2p=args.mode == "views-p2p")
             x_out.copy_(xp)
             return
         api.dmv3d_render_ddim_step(tp, intr, c2w, H, W, mlp, ab, t, tp_, x_in, None, 0.0, None,
@@ -369,7 +372,9 @@ def main():
                            "engine": engine_used,
                            "l2": "flushed between timed steps (256 MiB write); triplane re-read "
                                  "from HBM each step",
-                           "parallelism": (f"view-sharded x{world} (NCCL broadcast + all-gather)"
+                           "parallelism": (f"view-sharded x{world} (NCCL broadcast + "
+                                           + ("NVLink peer stores)" if args.mode == "views-p2p"
+                                              else "all-gather)")
                                            if views_mode else f"asset-sharded x{world}")},
                 "samples_per_s_nominal": value * w.samples_per_ray,
                 "samples_per_s_evaluated": eval_samples * world * args.steps / (total_ms / 1e3),

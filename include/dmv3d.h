@@ -129,6 +129,19 @@ typedef struct {
   float *plucker;          /* optional DEVICE [V][6][H][W]: the Plucker ray map
                               (o x d, d) of every rendered pixel,
                               written during ray generation; NULL = off              */
+  int32_t num_peers;       /* 0..7.  Every rgb / alpha / x_prev value this launch
+                              writes is also stored, at the same element offset, into
+                              each peer buffer below: P2P stores over NVLink into
+                              peer-mapped (e.g. symmetric-memory) buffers, so a view-
+                              sharded step assembles the full outputs on every GPU from
+                              the render epilogue itself (no separate all-gather).  The
+                              caller orders the peers' reads after this launch (a
+                              cross-GPU barrier).                                     */
+  float *const *peer_rgb;  /* HOST array [num_peers] of DEVICE pointers laid out like
+                              the rgb argument (NULL entry: skip that peer); same for
+                              alpha and x_prev.  The arrays may be NULL when unused.  */
+  float *const *peer_alpha;
+  float *const *peer_x_prev;
 } dmv3d_render_opts;
 
 /* Launch timer for measurement: each render call with opts.timer set records

@@ -53,7 +53,9 @@ class RenderOpts(ct.Structure):
                 ("ray_begin", ct.c_int64), ("ray_end", ct.c_int64), ("engine", ct.c_int32),
                 ("counters", ct.c_void_p), ("workspace", ct.c_void_p),
                 ("workspace_bytes", ct.c_uint64), ("timer", ct.c_void_p),
-                ("plucker", ct.c_void_p)]
+                ("plucker", ct.c_void_p), ("num_peers", ct.c_int32),
+                ("peer_rgb", ct.c_void_p), ("peer_alpha", ct.c_void_p),
+                ("peer_x_prev", ct.c_void_p)]
 
 
 class DdimParams(ct.Structure):

@@ -76,15 +76,29 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
                 term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None,
-                timer=None, plucker=None):
+                timer=None, plucker=None, peers=None):
+    """`peers`: optional dict with "rgb" / "alpha" / "x_prev" lists of device addresses
+    (ints, 0 = skip) laid out like the corresponding outputs (P2P copies, see the ABI)."""
     b, e = (-1, -1) if ray_range is None else ray_range
     ws_ptr = None if workspace is None else workspace.data_ptr()
     ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    return _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
-                           (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
-                           None if counters is None else counters.data_ptr(), ws_ptr, ws_len,
-                           None if timer is None else timer.handle,
-                           None if plucker is None else plucker.data_ptr())
+    o = _abi.RenderOpts(samples_per_ray, _AGG[agg], 1 if jitter else 0, seed,
+                        (ct.c_float * 3)(*bg), term_eps, b, e, _ENGINE[engine],
+                        None if counters is None else counters.data_ptr(), ws_ptr, ws_len,
+                        None if timer is None else timer.handle,
+                        None if plucker is None else plucker.data_ptr())
+    if peers:
+        n = max(len(peers.get(k) or []) for k in ("rgb", "alpha", "x_prev"))
+        arrs = {}
+        for k in ("rgb", "alpha", "x_prev"):
+            vals = list(peers.get(k) or []) + [0] * n
+            arrs[k] = (ct.c_void_p * n)(*[v or None for v in vals[:n]])
+        o.num_peers = n
+        o.peer_rgb = ct.cast(arrs["rgb"], ct.c_void_p)
+        o.peer_alpha = ct.cast(arrs["alpha"], ct.c_void_p)
+        o.peer_x_prev = ct.cast(arrs["x_prev"], ct.c_void_p)
+        o._keep = arrs  # the arrays must outlive the call
+    return o
 
 
 def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "DeviceMLP", grad_rgb,

@@ -134,6 +134,7 @@ dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
   if (o->counters) CHECK_ALIGN(o->counters, "opts.counters");
   if (o->workspace && (reinterpret_cast<uintptr_t>(o->workspace) & 255u))
     return fail(DMV3D_ERR_ALIGNMENT, "opts.workspace is not 256-byte aligned");
+  CHECK_ARG(o->num_peers >= 0 && o->num_peers <= kMaxPeers, "opts: num_peers must be in [0, 7]");
   return DMV3D_OK;
 }
 
@@ -185,6 +186,12 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.ws_bytes = o->workspace_bytes;
     P.timer = o->timer;
     P.plucker = o->plucker;
+    P.npeers = o->num_peers;
+    for (int k = 0; k < o->num_peers; ++k) {
+      P.peer_rgb[k] = o->peer_rgb ? o->peer_rgb[k] : nullptr;
+      P.peer_alpha[k] = o->peer_alpha ? o->peer_alpha[k] : nullptr;
+      P.peer_xp[k] = o->peer_x_prev ? o->peer_x_prev[k] : nullptr;
+    }
   }
 }
 

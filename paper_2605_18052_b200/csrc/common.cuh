@@ -15,6 +15,7 @@
 namespace dmv3d {
 
 constexpr int kMaxLayers = 8;
+constexpr int kMaxPeers = 7;  // the other GPUs of an 8-GPU node
 
 // All per-launch parameters; passed by value as a __grid_constant__.
 struct RenderParams {
@@ -59,6 +60,10 @@ struct RenderParams {
   void *timer;
   // optional Plucker ray map output [V][6][H][W] (row f2), written during a1
   float *plucker;
+  // P2P copies of every output value (view-sharded multi-GPU step): peer buffers laid
+  // out like rgb / alpha / x_prev
+  int32_t npeers;
+  float *peer_rgb[kMaxPeers], *peer_alpha[kMaxPeers], *peer_xp[kMaxPeers];
   // density grid mode of the tensor-core engine (row f3): G^3 points, x fastest
   int32_t grid_res;
   float *grid_sigma, *grid_rgb;
@@ -279,6 +284,20 @@ __device__ __forceinline__ void plucker_write(float *out, int H, int W, int v, i
   out[((int64_t)v * 6 + c) * HW + (int64_t)i * W + j] = plucker_component(ray, c);
 }
 
+// NVLink stores of one output value into the peers' buffers (out of line: keeps the
+// renderers' register allocation unchanged when no peers are given)
+static __device__ __noinline__ void peer_store_rgb(const RenderParams &P, int64_t irgb, int64_t ia, int ch,
+                                            float rgb, float a) {
+  for (int k = 0; k < P.npeers; ++k) {
+    if (P.peer_rgb[k]) P.peer_rgb[k][irgb] = rgb;
+    if (ch == 0 && P.peer_alpha[k]) P.peer_alpha[k][ia] = a;
+  }
+}
+static __device__ __noinline__ void peer_store_xp(const RenderParams &P, int64_t idx, float xp) {
+  for (int k = 0; k < P.npeers; ++k)
+    if (P.peer_xp[k]) P.peer_xp[k][idx] = xp;
+}
+
 // Per-ray epilogue: write rgb/alpha and, for DDIM views, x_{t-1}
 // (readings A15, A18-A20).  `ch` selects the channel this
 // thread writes (0..2); channel 0's thread also writes alpha.
@@ -287,8 +306,10 @@ __device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i
   const int64_t HW = (int64_t)P.H * P.W;
   const int64_t pix = (int64_t)i * P.W + j;
   const float out = c_val + T * P.bg[ch];
-  if (P.rgb) P.rgb[((int64_t)v * 3 + ch) * HW + pix] = out;
-  if (ch == 0 && P.alpha) P.alpha[(int64_t)v * HW + pix] = 1.0f - T;
+  const int64_t irgb = ((int64_t)v * 3 + ch) * HW + pix, ia = (int64_t)v * HW + pix;
+  if (P.rgb) P.rgb[irgb] = out;
+  if (ch == 0 && P.alpha) P.alpha[ia] = 1.0f - T;
+  if (P.npeers) peer_store_rgb(P, irgb, ia, ch, out, 1.0f - T);
   if (v < P.ddim_views) {
     const int64_t idx = ((int64_t)v * 3 + ch) * HW + pix;
     const float xt = __ldg(P.x_t + idx);
@@ -303,6 +324,7 @@ __device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i
         xp += P.sigma_t * (P.z ? __ldg(P.z + idx) : ddim_noise(P.noise_seed, (uint64_t)idx));
     }
     P.x_prev[idx] = xp;
+    if (P.npeers) peer_store_xp(P, idx, xp);
   }
 }
 

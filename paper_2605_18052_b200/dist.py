@@ -14,9 +14,15 @@ independent.  Two partitions are provided, in the priority order of §8e:
   4x4-patch rows, so the gathered result is bitwise equal to one GPU
   rendering all views (pin P12).
 
+* views with P2P outputs (`p2p=True`): the same split, but the outputs live in
+  symmetric memory (torch.distributed._symmetric_memory) and the render epilogue
+  itself stores every value into all peers' buffers over NVLink (opts.peers of the
+  ABI); one device-side barrier replaces the three all-gathers.
+
 The render call is injectable (`render_fn`) so the shard/merge logic is
 tested on CPU with gloo and the CPU oracle (tests/test_dist_gloo.py); the
-default is libdmv3d's fused step.
+default is libdmv3d's fused step.  The P2P path needs GPUs with peer access; its
+kernel side (peer stores) is tested on one GPU with local buffers as peers.
 """
 from __future__ import annotations
 
@@ -52,6 +58,26 @@ def _gather_views(full: torch.Tensor, v0: int, v1: int, per: int, world: int, gr
         dist.all_gather(parts, mine.clone(), group=group)
 
 
+def peer_pointers(base_ptrs, rank: int, offset_bytes: int) -> list[int]:
+    """Addresses of the same element in every other rank's symmetric buffer (bases in
+    rank order), in rank order skipping `rank`."""
+    return [int(b) + offset_bytes for r, b in enumerate(base_ptrs) if r != rank]
+
+
+_SYMM = {}
+
+
+def _symm_outputs(shapes, device, group):
+    """Symmetric-memory output tensors (cached per shape set) and their handles."""
+    import torch.distributed._symmetric_memory as symm_mem
+    key = (tuple(shapes), str(device), id(group))
+    if key not in _SYMM:
+        name = (group or dist.group.WORLD).group_name
+        ts = [symm_mem.empty(*shp, dtype=torch.float32, device=device) for shp in shapes]
+        _SYMM[key] = (ts, [symm_mem.rendezvous(t, name) for t in ts])
+    return _SYMM[key]
+
+
 def default_render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
                       x_t, x_prev, rgb, alpha, **opts):
     from . import api
@@ -65,13 +91,19 @@ def default_render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, 
 
 def denoise_step_view_sharded(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
                               x_t, ddim_views: int, group=None, src: int = 0,
-                              broadcast_triplane: bool = True, render_fn=None, **opts):
+                              broadcast_triplane: bool = True, render_fn=None, p2p: bool = False,
+                              **opts):
     """One denoising step of one asset, views split across the ranks of `group`.
 
     Every rank passes full-size `intrinsics` [V,4], `c2w` [V,3,4] and `x_t`
     [ddim_views,3,H,W] (only its own block is read).  Returns the full
     (x_prev [ddim_views,3,H,W], rgb [V,3,H,W], alpha [V,H,W]) on every rank.
+    `p2p`: outputs in symmetric memory, assembled by the render kernel's peer stores.
     """
+    if p2p and dist.get_world_size(group) > 1:
+        return _denoise_step_view_sharded_p2p(triplane, intrinsics, c2w, height, width, mlp,
+                                              alpha_bar, t, t_prev, x_t, ddim_views, group, src,
+                                              broadcast_triplane, render_fn, **opts)
     render_fn = render_fn or default_render_fn
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -95,6 +127,35 @@ def denoise_step_view_sharded(triplane, intrinsics, c2w, height, width, mlp, alp
         _gather_views(alpha, v0, v1, per, world, group)
         _gather_views(xp, v0, v1, per, world, group)
     return xp[:ddim_views], rgb[:V], alpha[:V]
+
+
+def _denoise_step_view_sharded_p2p(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t,
+                                   t_prev, x_t, ddim_views, group, src, broadcast_triplane,
+                                   render_fn, **opts):
+    render_fn = render_fn or default_render_fn
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    V = int(c2w.shape[0])
+    v0, v1 = view_shard(V, rank, world)
+    dev = triplane.device
+    if broadcast_triplane:
+        dist.broadcast(triplane, src=src, group=group)
+    (xp, rgb, alpha), (hx, hr, ha) = _symm_outputs(
+        [(max(ddim_views, 1), 3, height, width), (V, 3, height, width), (V, height, width)], dev,
+        group)
+    if v1 > v0:
+        own_dv = max(0, min(v1, ddim_views) - v0)
+        HW = height * width
+        peers = {"rgb": peer_pointers(hr.buffer_ptrs, rank, v0 * 3 * HW * 4),
+                 "alpha": peer_pointers(ha.buffer_ptrs, rank, v0 * HW * 4),
+                 "x_prev": peer_pointers(hx.buffer_ptrs, rank, v0 * 3 * HW * 4) if own_dv else []}
+        render_fn(triplane, intrinsics[v0:v1].contiguous(), c2w[v0:v1].contiguous(), height, width,
+                  mlp, alpha_bar, t, t_prev, x_t[v0:v0 + own_dv] if own_dv else None,
+                  xp[v0:v0 + own_dv] if own_dv else None, rgb[v0:v1], alpha[v0:v1], peers=peers,
+                  **opts)
+    # every rank's peer stores have landed once all ranks pass the device-side barrier
+    ha.barrier()
+    return xp[:ddim_views], rgb, alpha
 
 
 def max_over_ranks(value: float, device, group=None) -> float:

@@ -91,3 +91,12 @@ def test_view_shard_partition(V, P):
 def test_asset_shard_partition():
     owned = sorted(a for r in range(3) for a in pdist.asset_shard(8, r, 3))
     assert owned == list(range(8))
+
+
+def test_peer_pointers_skip_own_rank():
+    """P2P view sharding: each peer gets the same element offset in its own buffer."""
+    from paper_2605_18052_b200.dist import peer_pointers
+    bases = [1000, 5000, 9000, 13000]
+    assert peer_pointers(bases, 1, 64) == [1064, 9064, 13064]
+    assert peer_pointers(bases, 0, 0) == [5000, 9000, 13000]
+    assert peer_pointers([7], 0, 4) == []

@@ -133,3 +133,37 @@ def test_render_backward_matches_oracle(C, H, L, dtype, agg):
     for l in range(L):
         assert _close(dW[l].cpu().numpy(), oW[l]), l
         assert _close(db[l].cpu().numpy(), ob[l]), l
+
+
+@pytest.mark.parametrize("engine,dtype", [("simt", "f32"), ("tcgen05", "bf16")])
+def test_peer_stores_write_every_copy(engine, dtype):
+    """opts.peers (view-sharded multi-GPU step): every rgb / alpha / x_prev value the
+    render epilogue writes is also stored at the same offset of each peer buffer.  On one
+    GPU the peers are local buffers; the values must equal the local output bitwise."""
+    from paper_2605_18052_b200 import schedule
+    tp = wl.blob_triplane(12, 32, seed=2)
+    m = wl.blob_mlp(32, 64, 4, seed=3)
+    if dtype == "bf16":
+        tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
+    cams = wl.concat_cameras(wl.input_cameras(12, 10, 2), wl.novel_cameras(12, 10, 2, seed=4))
+    w = wl.Workload("peer", tp, cams, m, 24, dtype)
+    t, intr, c2w, mlp = dev_workload(w)
+    V, H, W = 4, 12, 10
+    x_t = torch.from_numpy(wl.gaussian((2, 3, H, W), 4)).cuda()
+    peer_rgb = [torch.full((V, 3, H, W), -1.0, device="cuda") for _ in range(3)]
+    peer_a = [torch.full((V, H, W), -1.0, device="cuda") for _ in range(3)]
+    peer_x = [torch.full((2, 3, H, W), -1.0, device="cuda") for _ in range(3)]
+    peers = {"rgb": [p.data_ptr() for p in peer_rgb], "alpha": [p.data_ptr() for p in peer_a],
+             "x_prev": [p.data_ptr() for p in peer_x[:2]] + [0]}  # third peer skips x_prev
+    xp, rgb, alpha = api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, schedule.cosine_alpha_bar(),
+                                                980, 960, x_t, samples_per_ray=24, engine=engine,
+                                                peers=peers)
+    for k in range(3):
+        assert torch.equal(peer_rgb[k], rgb) and torch.equal(peer_a[k], alpha)
+    assert torch.equal(peer_x[0], xp) and torch.equal(peer_x[1], xp)
+    assert (peer_x[2] == -1.0).all()
+    # a shard writes only its own rays, into the peers too (same offsets)
+    pr = torch.full((V, 3, H, W), -1.0, device="cuda")
+    api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=24, engine=engine,
+                           ray_range=(2 * H * W, 4 * H * W), peers={"rgb": [pr.data_ptr()]})
+    assert torch.equal(pr[2:], rgb[2:]) and (pr[:2] == -1.0).all()
