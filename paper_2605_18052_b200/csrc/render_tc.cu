@@ -87,6 +87,7 @@ struct TcShared {
   int patch[NG];
   int bbox[NG][2][8];  // per chunk parity: xmin,ymin,zmin,-,xmax,ymax,zmax,-
   int coltex[NG][kTcKMax];  // staged column -> texel index of G (-1: zero fill)
+  float head_bias[4];
 };
 
 template <int NG>
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       *reinterpret_cast<__half *>(wl + off) = __float2half_rn(v);
     }
   }
+  if (tid_cta < 4) sh->head_bias[tid_cta] = __ldg(P.b[L - 1] + tid_cta);
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -472,10 +474,14 @@ __global__ void __launch_bounds__(128 * NG, 1)
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
+          // the head skips its bias K block (4 FADDs at readout instead of an MMA)
+          const int nks = (l == L - 1) ? kTcHD / 16 : (int)kWK / 16;
 #pragma unroll
           for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
+            if (ks < nks) {
+              const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
+              ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
+            }
           }
           ptx::mma_commit(&sh->mbar[g]);
         }
@@ -491,12 +497,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ptx::tc_fence_before();
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
-        const float x = __uint_as_float(o4[0]) + P.dshift;
+        const float *bh = sh->head_bias;  // shared memory: broadcast reads
+        const float x = __uint_as_float(o4[0]) + bh[0] + P.dshift;
         sigma = __logf(1.0f + __expf(-fabsf(x))) + fmaxf(x, 0.0f);
         const float s = 1.0f + 2.0f * P.weps;
-        c0 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[1]))) - P.weps;
-        c1 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[2]))) - P.weps;
-        c2 = __fdividef(s, 1.0f + __expf(-__uint_as_float(o4[3]))) - P.weps;
+        c0 = __fdividef(s, 1.0f + __expf(-(__uint_as_float(o4[1]) + bh[1]))) - P.weps;
+        c1 = __fdividef(s, 1.0f + __expf(-(__uint_as_float(o4[2]) + bh[2]))) - P.weps;
+        c2 = __fdividef(s, 1.0f + __expf(-(__uint_as_float(o4[3]) + bh[3]))) - P.weps;
         n_samples++;
       }
       if constexpr (GRID) {
