@@ -152,3 +152,50 @@ def test_struct_layout_matches_header(tmp_path):
         assert got[(cname, "size")] == ct.sizeof(py), cname
         for f in py._fields_:
             assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
+
+
+def test_render_validation_fuzz():
+    """Random out-of-range mutations of valid arguments always come back as a documented
+    error status with a message -- never a crash, never OK -- before any device work."""
+    from hypothesis import given, settings, strategies as st
+
+    fields = {
+        ("t", "res"): st.integers(-3, 10000), ("t", "channels"): st.integers(-3, 300),
+        ("t", "sample_mode"): st.integers(-2, 3), ("t", "dtype"): st.integers(-1, 3),
+        ("m", "num_layers"): st.integers(-1, 12), ("m", "in_dim"): st.integers(-1, 300),
+        ("m", "hidden"): st.integers(-1, 300), ("m", "hidden_act"): st.integers(-1, 4),
+        ("c", "num_views"): st.integers(-1, 8), ("c", "height"): st.integers(-1, 8),
+        ("o", "samples_per_ray"): st.integers(-1, 2000), ("o", "agg"): st.integers(-1, 4),
+        ("o", "engine"): st.integers(-1, 4), ("o", "term_eps"): st.floats(-1.0, 2.0),
+        ("o", "num_peers"): st.integers(-1, 9),
+    }
+    valid_range = {"res": (2, 8192), "sample_mode": (0, 1), "dtype": (0, 1),
+                   "num_layers": (2, 8), "hidden_act": (0, 2), "num_views": (1, 1 << 30),
+                   "height": (1, 1 << 30), "samples_per_ray": (1, 1024), "agg": (0, 2),
+                   "engine": (0, 2), "num_peers": (0, 7), "channels": (1, 1 << 30)}
+    documented = {_abi.OK, _abi.ERR_INVALID_ARG, _abi.ERR_UNSUPPORTED, _abi.ERR_CUDA,
+                  _abi.ERR_ALIGNMENT}
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.lists(st.sampled_from(sorted(fields)), min_size=1, max_size=3, unique=True), st.data())
+    def run(keys, data):
+        keep = []
+        t, c, m, o = _valid_structs(keep)
+        objs = {"t": t, "c": c, "m": m, "o": o}
+        out_of_range = False
+        for k in keys:
+            v = data.draw(fields[k])
+            setattr(objs[k[0]], k[1], v)
+            lo, hi = valid_range.get(k[1], (-1e30, 1e30))
+            if k[1] == "term_eps":
+                lo, hi = 0.0, 0.999999
+            out_of_range |= not (lo <= v <= hi)
+        if not out_of_range:
+            return  # a valid call would launch on host pointers: only invalid ones are sent
+        rgb = np.zeros(64, np.float32)
+        s = _abi.lib().dmv3d_render_views(ct.byref(t), ct.byref(c), ct.byref(m), ct.byref(o),
+                                          rgb.ctypes.data, None, None)
+        assert s in documented and s != _abi.OK
+        assert len(_abi.lib().dmv3d_last_error()) > 0
+
+    run()
