@@ -353,6 +353,25 @@ def main():
                 "algorithmic": "(27,136 MLP + 1,920 gather) FLOP per evaluated sample"}
         dtype = "f32"
 
+    # ---- the gather's HBM roofline under both SURVEY.md §8d(iv) definitions: the
+    # triplane is L2-resident, so compulsory bytes (the triplane once per asset-step)
+    # are far below the HBM roof while the requested bytes (12 C elements per
+    # evaluated sample, what a per-sample gather reads) exceed it -- on-chip reuse
+    ks = kernel_ms / 1e3
+    req_b = 12 * w.triplane.shape[-1] * tp.element_size()
+    comp_b = tp.numel() * tp.element_size()
+    ncu = _ncu_traffic(engine_used) or 0
+    l2hit = _ncu_traffic(engine_used + "_l2_hit_pct")
+    gather = {"bound": "on-chip (L2-resident triplane)", "unit": "GB/s", "hbm_peak": peaks["hbm_gbs"],
+              "requested_bytes_per_sample": req_b,
+              "requested_gbs": eval_samples * req_b / ks / 1e9,
+              "requested_frac_of_hbm": eval_samples * req_b / ks / 1e9 / peaks["hbm_gbs"],
+              "compulsory_bytes_per_step": comp_b,
+              "compulsory_gbs": comp_b / ks / 1e9,
+              "compulsory_frac_of_hbm": comp_b / ks / 1e9 / peaks["hbm_gbs"],
+              "dram_gbs_ncu": ncu / ks / 1e9 if ncu else None,
+              "l2_hit_pct_ncu": l2hit}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -361,6 +380,10 @@ def main():
         cpu = {"value": r_rate, "unit": "rays/s", "cores": threads, "kind": "oracle",
                "sample": f"{n_rays} random rays of {args.config} (of {rays}) in {secs:.1f} s; full "
                          f"128-sample march, fp64, no early termination"}
+        # the oracle is also timed on one core
+        r1, n1, s1 = oracle_rate(w, args.cpu_budget / 3, 1, seed=8)
+        cpu["single_core"] = {"value": r1, "unit": "rays/s", "cores": 1,
+                              "sample": f"{n1} random rays of {args.config} in {s1:.1f} s"}
 
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "rays/s", "n_gpus": world,
@@ -381,7 +404,7 @@ def main():
                 "hit_fraction": hit_frac,
                 "terminated_fraction_of_hit": cnt[2] / max(cnt[0], 1),
                 "evaluated_fraction_of_nominal": eval_samples / (rays * w.samples_per_ray),
-                "roofline": roof, "cpu_baseline": cpu,
+                "roofline": roof, "gather_roofline": gather, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},
                 "gpu_launches": args.steps * launches_per_step,
