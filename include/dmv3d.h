@@ -156,7 +156,10 @@ dmv3d_status dmv3d_timer_reset(dmv3d_timer *timer);
 dmv3d_status dmv3d_timer_read(dmv3d_timer *timer, double *total_ms, int64_t *launches);
 
 /* Scratch the TCGEN05 engine needs for this triplane/MLP (0 if it cannot run
- * them): 256 + (3*R*R + 1)*hidden*2 bytes (the extra row holds b0). */
+ * them), enough for every TCGEN05 call: a 256-B header, the projected triplane
+ * G [(3*R*R + 1)][hidden] fp16 (the extra row holds b0) and, 256-B aligned after
+ * it, the backward's projected-space gradient dG [(3*R*R + 1)][hidden] fp32.
+ * Rendering alone needs only 256 + (3*R*R + 1)*hidden*2 bytes. */
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp);
 
 /* DDIM x0 -> x_{t-1} (readings A15-A20). */
@@ -216,8 +219,14 @@ dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_op
  * (opts.term_eps is ignored).  grad_rgb [V][3][H][W], grad_alpha [V][H][W] or
  * NULL; outputs are fp32 and ACCUMULATED (caller zeroes them): grad_triplane
  * [3][R][R][C], grad_weights / grad_biases = HOST arrays of L DEVICE pointers
- * shaped like W_l / b_l.  fp32 CUDA cores, ReLU hidden layers only; atomics make
- * the summation order, hence the last bits, run-dependent. */
+ * shaped like W_l / b_l.  ReLU hidden layers only; atomics make the summation
+ * order, hence the last bits, run-dependent.
+ * Engines: SIMT = fp32 CUDA cores (any supported shape).  TCGEN05 (also taken by
+ * AUTO when opts.workspace holds dmv3d_workspace_bytes()): bf16 triplane and
+ * weights, hidden 64, 2 <= L <= 7; the gradient of the first layer is accumulated
+ * in the projected space (dG = A^T dz0 on the tensor cores, then dF = dG W0,
+ * dW0 = dG^T F), activations and deltas are fp16 MMA operands with fp32
+ * accumulation.  The workspace is overwritten. */
 dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
                                    const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
                                    const float *grad_rgb, const float *grad_alpha,

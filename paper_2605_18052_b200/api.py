@@ -104,7 +104,8 @@ def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 
 def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "DeviceMLP", grad_rgb,
                           grad_alpha=None, aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, **opts):
     """Gradients of <grad_rgb, rgb> + <grad_alpha, alpha> w.r.t. the triplane and the MLP
-    (row f1) -> (d_triplane [3,R,R,C] f32, [dW_l] f32, [db_l] f32)."""
+    (row f1) -> (d_triplane [3,R,R,C] f32, [dW_l] f32, [db_l] f32).  engine="tcgen05" runs
+    the tensor-core backward (bf16 storage; a workspace is attached), otherwise fp32 SIMT."""
     dev = triplane.device
     dF = torch.zeros(triplane.shape, device=dev, dtype=torch.float32)
     dW = [torch.zeros(w.shape, device=dev, dtype=torch.float32) for w in mlp.weights]
@@ -113,6 +114,8 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
     t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
+    if opts.get("engine") == "tcgen05" and "workspace" not in opts:  # tensor-core backward
+        opts["workspace"] = workspace_for(t, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(**opts)
     L = len(dW)
     dWp = (ct.c_void_p * L)(*[x.data_ptr() for x in dW])

@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 
-SOURCES = ["api.cu", "render_simt.cu", "render_tc.cu", "elementwise.cu", "backward.cu"]
+SOURCES = ["api.cu", "render_simt.cu", "render_tc.cu", "elementwise.cu", "backward.cu", "backward_tc.cu"]
 HEADERS = ["common.cuh", "kernels.h", "tc_ptx.cuh", "simt_common.cuh"]
 
 

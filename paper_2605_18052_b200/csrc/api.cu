@@ -369,7 +369,27 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
   CHECK_ALIGN(grad_triplane, "grad_triplane");
   if (mlp->hidden_act != DMV3D_ACT_RELU)
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: ReLU hidden layers only");
-  if (!backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers, opts->agg == DMV3D_AGG_CONCAT))
+  // engine: the tensor-core backward needs bf16 storage, the TC engine's shapes and a
+  // workspace of dmv3d_workspace_bytes(); AUTO takes it when all hold
+  const bool tc_ok = triplane->dtype == DMV3D_BF16 && mlp->dtype == DMV3D_BF16 &&
+                     tc_backward_supported(triplane->channels, mlp->hidden, mlp->num_layers);
+  const bool ws_ok = opts->workspace &&
+                     opts->workspace_bytes >= tc_backward_workspace_bytes(triplane->res, mlp->hidden);
+  bool use_tc = false;
+  if (opts->engine == DMV3D_ENGINE_TCGEN05) {
+    if (!tc_ok)
+      return fail(DMV3D_ERR_UNSUPPORTED,
+                  "backward engine TCGEN05 needs bf16 triplane + weights, hidden 64, channels % 8 == 0 "
+                  "(<= 256), 2 <= L <= 7");
+    if (!ws_ok)
+      return fail(DMV3D_ERR_INVALID_ARG,
+                  "backward engine TCGEN05 needs opts.workspace of dmv3d_workspace_bytes() bytes");
+    use_tc = true;
+  } else if (opts->engine == DMV3D_ENGINE_AUTO && tc_ok && ws_ok) {
+    use_tc = true;
+  }
+  if (!use_tc &&
+      !backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers, opts->agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: unsupported (in_dim, hidden, L)");
   RenderParams P;
   fill_common(P, triplane, cams, mlp, opts);
@@ -382,6 +402,9 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
     G.dW[l] = grad_weights[l];
     G.db[l] = grad_biases[l];
   }
+  if (use_tc)
+    return cuda_status(launch_render_backward_tc(P, G, reinterpret_cast<cudaStream_t>(stream)),
+                       "backward (tcgen05) launch");
   return cuda_status(launch_render_backward(P, G, triplane->dtype == DMV3D_BF16,
                                             mlp->dtype == DMV3D_BF16,
                                             reinterpret_cast<cudaStream_t>(stream)),
@@ -480,7 +503,8 @@ dmv3d_status dmv3d_timer_read(dmv3d_timer *t, double *total_ms, int64_t *launche
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp) {
   if (!triplane || !mlp || triplane->res < 2) return 0;
   if (!tc_supported(triplane->channels, mlp->hidden, mlp->num_layers)) return 0;
-  return tc_workspace_bytes(triplane->res, mlp->hidden);
+  // enough for every tensor-core call: render (G) and backward (G + dG)
+  return tc_backward_workspace_bytes(triplane->res, mlp->hidden);
 }
 
 dmv3d_status dmv3d_render_views(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,

@@ -36,10 +36,18 @@ bool backward_supported(int K, int HD, int L, bool concat);
 cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, bool tp_bf16,
                                    bool w_bf16, cudaStream_t st);
 
-// render_tc.cu (tcgen05 / TMEM engine)
+// render_tc.cu (tcgen05 / TMEM engine).  Workspace: [256-B header: patch counter]
+// [G: (3 R R + 1) x HD fp16] (+ for the backward, 256-B aligned: [dG: (3 R R + 1) x HD fp32])
+constexpr uint32_t kTcWsHeader = 256;
 bool tc_supported(int C, int HD, int L);  // C = triplane channels per plane
 size_t tc_workspace_bytes(int R, int HD);
+cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st);
 cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
+
+// backward_tc.cu (row f1 on the tensor cores)
+size_t tc_backward_workspace_bytes(int R, int HD);
+bool tc_backward_supported(int C, int HD, int L);
+cudaError_t launch_render_backward_tc(const RenderParams &P, const GradParams &Gp, cudaStream_t st);
 
 // elementwise.cu
 struct DdimCoef {

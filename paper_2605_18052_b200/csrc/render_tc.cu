@@ -59,7 +59,7 @@ constexpr int kTcHD = 64;       // hidden width of the tensor-core engine
 constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
-constexpr uint32_t kWsHeader = 256;
+constexpr uint32_t kWsHeader = kTcWsHeader;
 
 // shared-memory carve-up (bytes)
 constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;    // 32 KiB, K-major, SBO 2048
@@ -603,21 +603,17 @@ static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cud
   return cudaGetLastError();
 }
 
-// P.grid_res > 0 selects the density-grid mode (row f3)
-cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
-  const bool grid_mode = P0.grid_res > 0;
-  if (!grid_mode && P0.ray_end <= P0.ray_begin) return cudaSuccess;
-  if (!P0.ws) return cudaErrorInvalidValue;
-  RenderParams P = P0;
+// K0 alone (shared with the tensor-core backward): G = F W0^T + b0 * bscale (fp16)
+// into the workspace, patch counter zeroed.  The bias is split over the three planes
+// except for the mean, whose A weights carry the 1/3; the half-pixel mode adds it
+// through the bias row instead.
+cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   uint8_t *ws = static_cast<uint8_t *>(P.ws);
   __half *G = reinterpret_cast<__half *>(ws + kWsHeader);
   unsigned int *counter = reinterpret_cast<unsigned int *>(ws);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // K0: G = F W0^T + b0 * bscale (fp16), zero the patch counter.  The bias is split
-  // over the three planes except for the mean, whose A weights carry the 1/3; the
-  // half-pixel mode adds it through the bias row instead.
   const int ntex = 3 * P.R * P.R;
   const size_t s0 = (size_t)kTcHD * P.C * 4;
   cudaError_t e = cudaFuncSetAttribute(preproject_kernel,
@@ -638,6 +634,22 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  return cudaSuccess;
+}
+
+// P.grid_res > 0 selects the density-grid mode (row f3)
+cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
+  const bool grid_mode = P0.grid_res > 0;
+  if (!grid_mode && P0.ray_end <= P0.ray_begin) return cudaSuccess;
+  if (!P0.ws) return cudaErrorInvalidValue;
+  RenderParams P = P0;
+  uint8_t *ws = static_cast<uint8_t *>(P.ws);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // K0: G = F W0^T + b0 * bscale (fp16), zero the patch counter
+  cudaError_t e = launch_preproject(P, st);
+  if (e != cudaSuccess) return e;
   // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
   const bool ng4 = tc_smem_bytes<4>(P.L) <= kSmemLimit;

@@ -122,6 +122,38 @@ def main():
                 "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
                              "frac": fl / FP32_PEAK,
                              "algorithmic": f"{per} FLOP per sample x ~0.95 hit x 128 samples"}})
+
+    # f1 on the tensor cores (engine tcgen05): same workload; whole call (memset, K0
+    # projection, the backward kernel, dF / dW0 maps) and the backward kernel alone
+    hit = api.dmv3d_debug_ray_geometry(intr, c2w, 128, 128)[2]
+    samples = int(hit.sum().item()) * 128
+
+    def f1tc(timer):
+        api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
+                                  timer=timer, engine="tcgen05")
+    k_ms = timed(f1tc, args.reps, flush)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    for _ in range(args.reps):
+        flush.zero_()
+        e0.record()
+        f1tc(None)
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    call_ms = tot / args.reps
+    # algorithmic work per sample: forward MLP + its transpose (dL/dh) + the weight
+    # gradients, 3 x 27,136 FLOP (the implementation's extra forward pass is not counted)
+    per_tc = 3 * 27136
+    fl = samples * per_tc / (k_ms / 1e3) / 1e12
+    bf = pk.get("bf16_tflops", 1654.5)
+    out.append({"row": "f1 renderer backward (tcgen05)", "metric": "rays/s",
+                "value": rays / (call_ms / 1e3), "call_ms": call_ms, "kernel_ms": k_ms,
+                "samples_per_s": samples / (call_ms / 1e3),
+                "config": "8 views 128^2, N=128, C=80, L=4, bf16 storage, fp16 MMAs",
+                "roofline": {"bound": "tensor", "achieved": fl, "peak": bf, "unit": "TFLOP/s",
+                             "frac": fl / bf, "kernel": "render_bwd_tc_kernel",
+                             "algorithmic": f"{per_tc} FLOP per sample x {samples} hit samples"}})
     for line in out:
         print(json.dumps(line))
 
