@@ -142,6 +142,11 @@ typedef struct {
                               alpha and x_prev.  The arrays may be NULL when unused.  */
   float *const *peer_alpha;
   float *const *peer_x_prev;
+  const float *fwd_rgb;    /* backward only, optional DEVICE [V][3][H][W] / [V][H][W]: the  */
+  const float *fwd_alpha;  /* forward render of the same call (rgb, alpha; term_eps 0, or
+                              within term_eps).  Given both, the backward takes C = rgb
+                              and T_N = 1 - alpha from them instead of marching every
+                              ray a first time (training has them from its forward).  */
 } dmv3d_render_opts;
 
 /* Launch timer for measurement: each render call with opts.timer set records

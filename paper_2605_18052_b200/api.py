@@ -76,9 +76,10 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
                 term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None,
-                timer=None, plucker=None, peers=None):
+                timer=None, plucker=None, peers=None, fwd=None):
     """`peers`: optional dict with "rgb" / "alpha" / "x_prev" lists of device addresses
-    (ints, 0 = skip) laid out like the corresponding outputs (P2P copies, see the ABI)."""
+    (ints, 0 = skip) laid out like the corresponding outputs (P2P copies, see the ABI).
+    `fwd`: (rgb, alpha) of the forward render, for the backward (opts.fwd_rgb / fwd_alpha)."""
     b, e = (-1, -1) if ray_range is None else ray_range
     ws_ptr = None if workspace is None else workspace.data_ptr()
     ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
@@ -87,6 +88,8 @@ def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 
                         None if counters is None else counters.data_ptr(), ws_ptr, ws_len,
                         None if timer is None else timer.handle,
                         None if plucker is None else plucker.data_ptr())
+    if fwd is not None:
+        o.fwd_rgb, o.fwd_alpha = fwd[0].data_ptr(), fwd[1].data_ptr()
     if peers:
         n = max(len(peers.get(k) or []) for k in ("rgb", "alpha", "x_prev"))
         arrs = {}

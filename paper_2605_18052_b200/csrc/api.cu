@@ -397,6 +397,14 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
   G.g_rgb = grad_rgb;
   G.g_alpha = grad_alpha;
   G.dF = grad_triplane;
+  CHECK_ARG((opts->fwd_rgb == nullptr) == (opts->fwd_alpha == nullptr),
+            "backward: give both opts.fwd_rgb and opts.fwd_alpha, or neither");
+  if (opts->fwd_rgb) {
+    CHECK_ALIGN(opts->fwd_rgb, "opts.fwd_rgb");
+    CHECK_ALIGN(opts->fwd_alpha, "opts.fwd_alpha");
+  }
+  G.fwd_rgb = opts->fwd_rgb;
+  G.fwd_alpha = opts->fwd_alpha;
   for (int l = 0; l < mlp->num_layers; ++l) {
     CHECK_ARG(grad_weights[l] && grad_biases[l], "backward: a gradient layer pointer is NULL");
     G.dW[l] = grad_weights[l];

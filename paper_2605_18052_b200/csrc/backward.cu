@@ -89,9 +89,16 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     const float gA = Gp.g_alpha ? __ldg(Gp.g_alpha + (int64_t)v * HWp + pix) : 0.0f;
     const float delta = sample_delta(ray, P.N);
 
-    // ---- pass 1: C and T_N
+    // ---- pass 1: C and T_N (or the caller's forward render)
     float Tc = 1.0f, acc[3] = {0.f, 0.f, 0.f};
-    for (int k0 = 0; k0 < P.N; k0 += 32) {
+    const bool have_fwd = Gp.fwd_rgb != nullptr;
+    if (have_fwd) {
+      Tc = 1.0f - __ldg(Gp.fwd_alpha + (int64_t)v * HWp + pix);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)  // C = acc + Tc bg below (acc summed over the warp)
+        acc[c] = lane == 0 ? __ldg(Gp.fwd_rgb + ((int64_t)v * 3 + c) * HWp + pix) - Tc * P.bg[c] : 0.0f;
+    }
+    for (int k0 = 0; k0 < (have_fwd ? 0 : P.N); k0 += 32) {
       const int k = k0 + lane;
       const bool valid = k < P.N;
       float sigma = 0.0f, c[3] = {0.f, 0.f, 0.f};

@@ -432,9 +432,19 @@ __global__ void __launch_bounds__(128 * NG, 1)
       for (int c = 0; c < 4; ++c) o[c] = __uint_as_float(o4[c]) + sh->head_bias[c];
     };
 
-    // ---------------- pass 1: C and T_N of every ray
+    // ---------------- pass 1: C and T_N of every ray (or the caller's forward render)
     float T = 1.0f, acc[3] = {0.f, 0.f, 0.f};
-    for (int k0 = 0; k0 < P.N; k0 += kChunk) {
+    const bool have_fwd = Gp.fwd_rgb != nullptr;
+    if (have_fwd && alive) {
+      const int64_t px = (int64_t)i * P.W + j;
+#pragma unroll
+      for (int e = 0; e < 3; ++e)  // C = acc + T bg below, with acc := C - bg T_N
+        acc[e] = __ldg(Gp.fwd_rgb + ((int64_t)v * 3 + e) * HW + px);
+      T = 1.0f - __ldg(Gp.fwd_alpha + (int64_t)v * HW + px);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) acc[e] = q == 0 ? acc[e] - T * P.bg[e] : 0.0f;
+    }
+    for (int k0 = 0; k0 < (have_fwd ? 0 : P.N); k0 += kChunk) {
       float o[4];
       forward(k0, o);
       float sigma = 0.0f, c[3] = {0.f, 0.f, 0.f};

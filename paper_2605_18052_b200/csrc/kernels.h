@@ -31,6 +31,8 @@ struct GradParams {
   float *dF;             // [3][R][R][C], fp32, accumulated
   float *dW[kMaxLayers];  // [out][in], accumulated
   float *db[kMaxLayers];  // [out], accumulated
+  const float *fwd_rgb;   // optional forward render (C per ray) ...
+  const float *fwd_alpha; // ... and alpha (T_N = 1 - alpha): skips the first march
 };
 bool backward_supported(int K, int HD, int L, bool concat);
 cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, bool tp_bf16,

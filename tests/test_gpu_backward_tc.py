@@ -137,3 +137,26 @@ def test_backward_tc_accumulates_into_caller_buffers_and_is_stable():
     assert _rel_err(a[0], b[0]) < 1e-5
     for l in range(4):
         assert _rel_err(a[1][l], b[1][l]) < 1e-5
+
+
+@pytest.mark.parametrize("engine,rel", [("tcgen05", REL), ("simt", 1e-4)])
+def test_backward_from_forward_outputs(engine, rel):
+    """opts.fwd_rgb / fwd_alpha: the backward takes C and T_N from the caller's forward
+    render (no first march) and reaches the same gradients."""
+    C, L, H, W, N = 32, 4, 10, 9, 40
+    tp = wl.round_to_bf16(wl.blob_triplane(12, C, seed=7, kappa=4.0))
+    m = wl.bf16_mlp(wl.blob_mlp(C, 64, L, seed=8))
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 2), wl.novel_cameras(H, W, 1, seed=9))
+    t, intr, c2w, mlp = dev_workload(wl.Workload("bwf", tp, cams, m, N, "bf16"))
+    rng = np.random.default_rng(3)
+    g = rng.normal(size=(3, 3, H, W)).astype(np.float32)
+    gA = rng.normal(size=(3, H, W)).astype(np.float32)
+    bg = (0.3, 0.5, 0.7)
+    rgb, alpha = api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=N, bg=bg,
+                                        engine=engine)
+    dF, dW, db = api.dmv3d_render_backward(t, intr, c2w, H, W, mlp, torch.from_numpy(g).cuda(),
+                                           torch.from_numpy(gA).cuda(), samples_per_ray=N, bg=bg,
+                                           engine=engine, fwd=(rgb, alpha))
+    oF, oW, ob = oracle.render_backward(tp, cams, m, N, g, gA, bg=bg)
+    _check((dF.cpu().numpy(), [x.cpu().numpy() for x in dW], [x.cpu().numpy() for x in db],
+            oF, oW, ob), rel=rel)

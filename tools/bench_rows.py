@@ -132,16 +132,34 @@ def main():
         api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
                                   timer=timer, engine="tcgen05")
     k_ms = timed(f1tc, args.reps, flush)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tot = 0.0
-    for _ in range(args.reps):
-        flush.zero_()
-        e0.record()
-        f1tc(None)
-        e1.record()
-        torch.cuda.synchronize()
-        tot += e0.elapsed_time(e1)
-    call_ms = tot / args.reps
+
+    def call_time(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(args.reps):
+            flush.zero_()
+            e0.record()
+            fn(None)
+            e1.record()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot / args.reps
+    call_ms = call_time(f1tc)
+    # training-step form: the forward render (term_eps 0) is already there, its rgb /
+    # alpha replace the backward's first march (opts.fwd_rgb / fwd_alpha)
+    rgb, alpha = api.dmv3d_render_views(tp, intr, c2w, 128, 128, mlp, samples_per_ray=128,
+                                        engine="tcgen05")
+
+    def f1tc_fwd(timer):
+        api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
+                                  timer=timer, engine="tcgen05", fwd=(rgb, alpha))
+
+    def fwd_only(timer):
+        api.dmv3d_render_views(tp, intr, c2w, 128, 128, mlp, rgb=rgb, alpha=alpha,
+                               samples_per_ray=128, engine="tcgen05", timer=timer)
+    kf_ms = timed(f1tc_fwd, args.reps, flush)
+    callf_ms = call_time(f1tc_fwd)
+    fwd_ms = call_time(fwd_only)
     # algorithmic work per sample: forward MLP + its transpose (dL/dh) + the weight
     # gradients, 3 x 27,136 FLOP (the implementation's extra forward pass is not counted)
     per_tc = 3 * 27136
@@ -153,6 +171,15 @@ def main():
                 "config": "8 views 128^2, N=128, C=80, L=4, bf16 storage, fp16 MMAs",
                 "roofline": {"bound": "tensor", "achieved": fl, "peak": bf, "unit": "TFLOP/s",
                              "frac": fl / bf, "kernel": "render_bwd_tc_kernel",
+                             "algorithmic": f"{per_tc} FLOP per sample x {samples} hit samples"}})
+    fl2 = samples * per_tc / (kf_ms / 1e3) / 1e12
+    out.append({"row": "f1 renderer backward (tcgen05, given the forward's rgb/alpha)",
+                "metric": "rays/s", "value": rays / (callf_ms / 1e3), "call_ms": callf_ms,
+                "kernel_ms": kf_ms, "forward_render_ms": fwd_ms,
+                "forward_plus_backward_rays_per_s": rays / ((fwd_ms + callf_ms) / 1e3),
+                "config": "as above; opts.fwd_rgb / fwd_alpha from a term_eps = 0 forward",
+                "roofline": {"bound": "tensor", "achieved": fl2, "peak": bf, "unit": "TFLOP/s",
+                             "frac": fl2 / bf, "kernel": "render_bwd_tc_kernel",
                              "algorithmic": f"{per_tc} FLOP per sample x {samples} hit samples"}})
     for line in out:
         print(json.dumps(line))
