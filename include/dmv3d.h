@@ -58,7 +58,9 @@ typedef enum {
   DMV3D_ERR_ALIGNMENT = 4    /* a tensor pointer is not 16-byte aligned         */
 } dmv3d_status;
 
-typedef enum { DMV3D_F32 = 0, DMV3D_BF16 = 1 } dmv3d_dtype;
+/* FP8_E4M3: triplane storage only (row f4), value = fp8_scale * e4m3 (OCP E4M3,
+ * finite range +-448), TCGEN05 engine only (its pre-projection decodes it). */
+typedef enum { DMV3D_F32 = 0, DMV3D_BF16 = 1, DMV3D_FP8_E4M3 = 2 } dmv3d_dtype;
 /* A4; CONCAT (row f4) feeds [f_XY, f_XZ, f_YZ] (in_dim = 3 C) to the MLP */
 typedef enum { DMV3D_AGG_MEAN = 0, DMV3D_AGG_SUM = 1, DMV3D_AGG_CONCAT = 2 } dmv3d_agg;
 /* Texel addressing (A3).  ALIGN_CORNERS: texel centres at the box faces, clamped
@@ -84,11 +86,14 @@ typedef struct {
 
 /* Triplane S_t (reading A1: R = 64, C = 32 or 80). */
 typedef struct {
-  int32_t res, channels; /* R >= 2; C >= 1 (C % 4 == 0 for F32, C % 8 == 0 for BF16) */
+  int32_t res, channels; /* R >= 2; C >= 1 (C % 4 == 0 for F32, C % 8 == 0 for BF16,
+                            C % 16 == 0 for FP8_E4M3)                              */
   dmv3d_dtype dtype;
   const void *data;      /* [3][R][R][C] DEVICE                                   */
   float aabb_min[3], aabb_max[3]; /* object box, default -1/+1    */
   dmv3d_sample_mode sample_mode;  /* texel addressing, default ALIGN_CORNERS         */
+  float fp8_scale;       /* FP8_E4M3 dequantisation scale (0 is read as 1); ignored
+                            for the other dtypes                                    */
 } dmv3d_triplane;
 
 /* Shared MLP decoder (reading A5-A7).  Layer l maps

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DMV3D_LIB") or os.path.join(HERE, "libdmv3d.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_ALIGNMENT = 0, 1, 2, 3, 4
-F32, BF16 = 0, 1
+F32, BF16, FP8_E4M3 = 0, 1, 2
 AGG_MEAN, AGG_SUM, AGG_CONCAT = 0, 1, 2
 SAMPLE_ALIGN_CORNERS, SAMPLE_HALFPIXEL_ZEROS = 0, 1
 ACT_RELU, ACT_SILU, ACT_SOFTPLUS = 0, 1, 2
@@ -37,7 +37,7 @@ class Cameras(ct.Structure):
 class Triplane(ct.Structure):
     _fields_ = [("res", ct.c_int32), ("channels", ct.c_int32), ("dtype", ct.c_int32),
                 ("data", ct.c_void_p), ("aabb_min", ct.c_float * 3), ("aabb_max", ct.c_float * 3),
-                ("sample_mode", ct.c_int32)]
+                ("sample_mode", ct.c_int32), ("fp8_scale", ct.c_float)]
 
 
 class MLP(ct.Structure):

@@ -60,12 +60,14 @@ class DeviceMLP:
 
 
 def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0, 1.0, 1.0),
-                    sample_mode="align_corners"):
+                    sample_mode="align_corners", fp8_scale=1.0):
+    """`tp` float32 / bfloat16 / float8_e4m3fn (value = fp8_scale * e4m3, TCGEN05 only)."""
     assert tp.dim() == 4 and tp.shape[0] == 3 and tp.shape[1] == tp.shape[2] and tp.is_contiguous()
-    dt = {torch.float32: _abi.F32, torch.bfloat16: _abi.BF16}[tp.dtype]
+    dt = {torch.float32: _abi.F32, torch.bfloat16: _abi.BF16,
+          torch.float8_e4m3fn: _abi.FP8_E4M3}[tp.dtype]
     return _abi.Triplane(int(tp.shape[1]), int(tp.shape[3]), dt, tp.data_ptr(),
                          (ct.c_float * 3)(*aabb_min), (ct.c_float * 3)(*aabb_max),
-                         _SMODE[sample_mode])
+                         _SMODE[sample_mode], fp8_scale)
 
 
 def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, width: int):
@@ -114,7 +116,8 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
     dW = [torch.zeros(w.shape, device=dev, dtype=torch.float32) for w in mlp.weights]
     db = [torch.zeros(b.shape, device=dev, dtype=torch.float32) for b in mlp.biases]
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
+    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                        fp8_scale=opts.pop("fp8_scale", 1.0))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     if opts.get("engine") == "tcgen05" and "workspace" not in opts:  # tensor-core backward
@@ -133,14 +136,14 @@ def dmv3d_render_backward(triplane, intrinsics, c2w, height, width, mlp: "Device
 
 def dmv3d_density_grid(triplane, mlp: "DeviceMLP", grid_res, want_rgb=True, agg="mean",
                        aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, timer=None, engine="auto",
-                       sample_mode="align_corners"):
+                       sample_mode="align_corners", fp8_scale=1.0):
     """sigma [G,G,G] (+ rgb [3,G,G,G]) of the decoder on the box grid."""
     G = int(grid_res)
     dev = triplane.device
     sigma = torch.empty((G, G, G), device=dev, dtype=torch.float32)
     rgb = torch.empty((3, G, G, G), device=dev, dtype=torch.float32) if want_rgb else None
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max, sample_mode)
+    t = triplane_struct(triplane, aabb_min, aabb_max, sample_mode, fp8_scale)
     m = mlp.struct(keep)
     ws = workspace_for(t, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(agg=agg, engine=engine, workspace=ws, timer=timer)
@@ -232,7 +235,8 @@ def dmv3d_render_views(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
     if alpha is None:
         alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
     keep = []
-    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
+    t = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                        fp8_scale=opts.pop("fp8_scale", 1.0))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     if "workspace" not in opts:
@@ -273,7 +277,8 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
     if alpha is None and want_alpha:
         alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
     keep = []
-    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"))
+    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                        fp8_scale=opts.pop("fp8_scale", 1.0))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     if "workspace" not in opts:
@@ -312,7 +317,8 @@ def dmv3d_render_ddim_step_host(ws: Workspace, triplane, intrinsics, c2w, height
     """Host-buffer step: every tensor is a (pinned) CPU tensor; copies in/out are inside
     the library call, on `stream` (default: torch's current stream)."""
     keep = []
-    tt = triplane_struct(triplane, sample_mode=opts.pop("sample_mode", "align_corners"))
+    tt = triplane_struct(triplane, sample_mode=opts.pop("sample_mode", "align_corners"),
+                        fp8_scale=opts.pop("fp8_scale", 1.0))
     c = cameras_struct(intrinsics, c2w, height, width)
     m = mlp.struct(keep)
     o = opts_struct(**opts)

@@ -83,7 +83,9 @@ dmv3d_status check_triplane(const dmv3d_triplane *t) {
   CHECK_ARG(t != nullptr, "triplane is NULL");
   CHECK_ARG(t->res >= 2 && t->res <= 8192, "triplane: res must be in [2, 8192]");
   CHECK_ARG(t->channels >= 1, "triplane: channels must be >= 1");
-  CHECK_ARG(t->dtype == DMV3D_F32 || t->dtype == DMV3D_BF16, "triplane: bad dtype");
+  CHECK_ARG(t->dtype == DMV3D_F32 || t->dtype == DMV3D_BF16 || t->dtype == DMV3D_FP8_E4M3,
+            "triplane: bad dtype");
+  CHECK_ARG(isfinite(t->fp8_scale), "triplane: non-finite fp8_scale");
   CHECK_ARG(t->data != nullptr, "triplane: data is NULL");
   CHECK_ALIGN(t->data, "triplane.data");
   CHECK_ARG(t->sample_mode == DMV3D_SAMPLE_ALIGN_CORNERS || t->sample_mode == DMV3D_SAMPLE_HALFPIXEL_ZEROS,
@@ -92,6 +94,8 @@ dmv3d_status check_triplane(const dmv3d_triplane *t) {
     return fail(DMV3D_ERR_UNSUPPORTED, "triplane: fp32 needs channels % 4 == 0 (16-byte vectors)");
   if (t->dtype == DMV3D_BF16 && t->channels % 8)
     return fail(DMV3D_ERR_UNSUPPORTED, "triplane: bf16 needs channels % 8 == 0 (16-byte vectors)");
+  if (t->dtype == DMV3D_FP8_E4M3 && t->channels % 16)
+    return fail(DMV3D_ERR_UNSUPPORTED, "triplane: fp8 needs channels % 16 == 0 (16-byte vectors)");
   return check_aabb(t->aabb_min, t->aabb_max);
 }
 
@@ -150,6 +154,8 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
   P.C = t->channels;
   P.tp = t->data;
   P.smode = t->sample_mode;
+  P.tp_fp8 = t->dtype == DMV3D_FP8_E4M3 ? 1 : 0;
+  P.tp_scale = (t->dtype == DMV3D_FP8_E4M3 && t->fp8_scale != 0.0f) ? t->fp8_scale : 1.0f;
   for (int a = 0; a < 3; ++a) {
     P.lo[a] = t->aabb_min[a];
     P.hi[a] = t->aabb_max[a];
@@ -230,7 +236,7 @@ enum class Engine { SIMT, TC };
 
 dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3d_render_opts *o,
                          Engine &e) {
-  const bool bf16 = t->dtype == DMV3D_BF16 && m->dtype == DMV3D_BF16;
+  const bool bf16 = (t->dtype == DMV3D_BF16 || t->dtype == DMV3D_FP8_E4M3) && m->dtype == DMV3D_BF16;
   const bool tc_ok = bf16 && m->hidden_act == DMV3D_ACT_RELU &&
                      tc_supported(t->channels, m->hidden, m->num_layers);
   const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden);
@@ -249,6 +255,9 @@ dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3
     e = Engine::TC;
     return DMV3D_OK;
   }
+  if (t->dtype == DMV3D_FP8_E4M3)
+    return fail(DMV3D_ERR_UNSUPPORTED, "fp8 triplane storage needs engine TCGEN05 (bf16 weights, "
+                                       "hidden 64, a workspace)");
   if (!simt_supported(m->in_dim, m->hidden, o->agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "SIMT engine: unsupported (in_dim, hidden) = (" +
                                            std::to_string(m->in_dim) + ", " + std::to_string(m->hidden) + ")");
@@ -371,7 +380,8 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: ReLU hidden layers only");
   // engine: the tensor-core backward needs bf16 storage, the TC engine's shapes and a
   // workspace of dmv3d_workspace_bytes(); AUTO takes it when all hold
-  const bool tc_ok = triplane->dtype == DMV3D_BF16 && mlp->dtype == DMV3D_BF16 &&
+  const bool tc_ok = (triplane->dtype == DMV3D_BF16 || triplane->dtype == DMV3D_FP8_E4M3) &&
+                     mlp->dtype == DMV3D_BF16 &&
                      tc_backward_supported(triplane->channels, mlp->hidden, mlp->num_layers);
   const bool ws_ok = opts->workspace &&
                      opts->workspace_bytes >= tc_backward_workspace_bytes(triplane->res, mlp->hidden);
@@ -388,6 +398,8 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
   } else if (opts->engine == DMV3D_ENGINE_AUTO && tc_ok && ws_ok) {
     use_tc = true;
   }
+  if (!use_tc && triplane->dtype == DMV3D_FP8_E4M3)
+    return fail(DMV3D_ERR_UNSUPPORTED, "backward: fp8 triplane storage needs engine TCGEN05");
   if (!use_tc &&
       !backward_supported(mlp->in_dim, mlp->hidden, mlp->num_layers, opts->agg == DMV3D_AGG_CONCAT))
     return fail(DMV3D_ERR_UNSUPPORTED, "backward: unsupported (in_dim, hidden, L)");
@@ -617,6 +629,8 @@ dmv3d_status dmv3d_debug_sample_features(const dmv3d_triplane *triplane, dmv3d_a
   if ((s = check_agg(agg)) != DMV3D_OK) return s;
   CHECK_ARG(n >= 0, "n must be >= 0");
   CHECK_ARG(n == 0 || (points && feats), "points / feats is NULL");
+  if (triplane->dtype == DMV3D_FP8_E4M3)
+    return fail(DMV3D_ERR_UNSUPPORTED, "debug entry points are SIMT: no fp8 triplane storage");
   if (n) {
     CHECK_ALIGN(points, "points");
     CHECK_ALIGN(feats, "feats");
@@ -642,6 +656,8 @@ dmv3d_status dmv3d_debug_decode(const dmv3d_triplane *triplane, const dmv3d_mlp 
   if ((s = check_mlp(mlp, triplane, agg)) != DMV3D_OK) return s;
   CHECK_ARG(n >= 0, "n must be >= 0");
   CHECK_ARG(n == 0 || (points && sigma_rgb), "points / sigma_rgb is NULL");
+  if (triplane->dtype == DMV3D_FP8_E4M3)
+    return fail(DMV3D_ERR_UNSUPPORTED, "debug entry points are SIMT: no fp8 triplane storage");
   if (n) {
     CHECK_ALIGN(points, "points");
     CHECK_ALIGN(sigma_rgb, "sigma_rgb");
@@ -715,7 +731,7 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t V = cams->num_views, HW = (size_t)cams->height * cams->width;
   const size_t tp_bytes = (size_t)3 * triplane->res * triplane->res * triplane->channels *
-                          (triplane->dtype == DMV3D_BF16 ? 2 : 4);
+                          (triplane->dtype == DMV3D_F32 ? 4 : triplane->dtype == DMV3D_BF16 ? 2 : 1);
   const size_t img_in = (size_t)ddim->ddim_views * 3 * HW * 4;
   cudaError_t e = cudaSuccess;
 #define TRY(x)                                                  \

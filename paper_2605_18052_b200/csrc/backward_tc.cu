@@ -39,6 +39,7 @@
 // No early termination (opts.term_eps is ignored): the gradient is exact up to the
 // fp16 operand rounding (tolerances).
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -689,8 +690,9 @@ __global__ void __launch_bounds__(256)
 // tid / 64) owns columns c = part, part + 4, ... (< C + 1; column C = the bias).
 constexpr int kWgTex = 32;
 constexpr int kWgMaxCols = 65;  // ceil((256 + 1) / 4)
+template <bool FP8>
 __global__ void __launch_bounds__(256)
-    bwd_dw0_kernel(const float *__restrict__ dG, const __nv_bfloat16 *__restrict__ F, int C,
+    bwd_dw0_kernel(const float *__restrict__ dG, const void *__restrict__ Fv, float fscale, int C,
                    int R, int cat, int wstride, float bscale, int bias_row, float *__restrict__ dW0,
                    float *__restrict__ db0, int tex_per_block) {
   __shared__ float sg[kWgTex][kHD];
@@ -710,7 +712,17 @@ __global__ void __launch_bounds__(256)
     for (int e = tid; e < nt * kHD; e += 256) sg[e / kHD][e % kHD] = dG[(tb + e / kHD) * kHD + e % kHD];
     for (int e = tid; e < nt * (C + 1); e += 256) {
       const int tt = e / (C + 1), c = e - tt * (C + 1);
-      sf[tt][c] = c < C ? __bfloat162float(F[(tb + tt) * C + c]) : bscale;
+      float fv = bscale;
+      if (c < C) {
+        if constexpr (FP8) {
+          const __half_raw hr = __nv_cvt_fp8_to_halfraw(
+              static_cast<const __nv_fp8_storage_t *>(Fv)[(tb + tt) * C + c], __NV_E4M3);
+          fv = fscale * __half2float(__half(hr));
+        } else {
+          fv = __bfloat162float(static_cast<const __nv_bfloat16 *>(Fv)[(tb + tt) * C + c]);
+        }
+      }
+      sf[tt][c] = fv;
     }
     __syncthreads();
     for (int tt = 0; tt < nt; ++tt) {
@@ -784,8 +796,8 @@ cudaError_t launch_render_backward_tc(const RenderParams &P0, const GradParams &
   int tpb = (int)((3 * RR + 2 * sms - 1) / (2 * sms));
   while (RR % tpb) ++tpb;
   const float bscale = P.smode != 0 ? 0.0f : (P.agg == 0 ? 1.0f : (1.0f / 3.0f));
-  bwd_dw0_kernel<<<(int)((3 * RR) / tpb), 256, 0, st>>>(
-      dG, reinterpret_cast<const __nv_bfloat16 *>(P.tp), C, R, cat ? 1 : 0, wstride, bscale,
+  (P.tp_fp8 ? bwd_dw0_kernel<true> : bwd_dw0_kernel<false>)<<<(int)((3 * RR) / tpb), 256, 0, st>>>(
+      dG, P.tp, P.tp_scale, C, R, cat ? 1 : 0, wstride, bscale,
       P.smode != 0 ? 1 : 0, Gp.dW[0], Gp.db[0], tpb);
   return cudaGetLastError();
 }

@@ -29,6 +29,8 @@ struct RenderParams {
   float lo[3], hi[3];
   float inv_ext[3];  // 1/(hi-lo) if a power of two, else 0 (see texel_coord)
   int32_t smode;     // texel addressing: 0 align-corners/clamp, 1 half-pixel/zeros (f4)
+  int32_t tp_fp8;    // storage FP8 E4M3 (value = tp_scale * e4m3; TC engine only, f4)
+  float tp_scale;
   // shared MLP
   int32_t L, K, HD;
   const void *w[kMaxLayers];

@@ -29,6 +29,7 @@
 //    The NG groups interleave on the SM: while one group waits on its MMA
 //    chain the others stage, scatter and run epilogues.
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -102,10 +103,12 @@ static size_t tc_smem_bytes(int L) {
 // W0 rows have stride `wstride` (3 C for the concat aggregation, whose planes are
 // projected by their own column block of W0).  Optionally zeroes the patch counter
 // and writes fp16(b0) to `gbias` (the bias row of the half-pixel mode).
+// FP8: F is E4M3 storage (row f4) dequantised by `fscale`; 16 channels per 16-B load.
+template <bool FP8>
 __global__ void __launch_bounds__(256)
-    preproject_kernel(const __nv_bfloat16 *__restrict__ F, int ntex, int C, int wstride,
+    preproject_kernel(const void *__restrict__ Fv, int ntex, int C, int wstride,
                       const __nv_bfloat16 *__restrict__ W0, const float *__restrict__ b0,
-                      float bscale, __half *__restrict__ G, unsigned int *counter,
+                      float bscale, float fscale, __half *__restrict__ G, unsigned int *counter,
                       __half *__restrict__ gbias) {
   extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
   for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {
@@ -121,17 +124,39 @@ __global__ void __launch_bounds__(256)
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntex;
        t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     float a0 = bias0, a1 = bias1;
-    const uint4 *src = reinterpret_cast<const uint4 *>(F + t * C);
-    for (int q = 0; q < C / 8; ++q) {
-      const uint4 u = __ldg(src + q);  // same address across the warp: one broadcast request
-      const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
+    if constexpr (FP8) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint8_t *>(Fv) + t * C);
+      float s0 = 0.0f, s1 = 0.0f;
+      for (int q = 0; q < C / 16; ++q) {
+        const uint4 u = __ldg(src + q);
+        const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 w0 = swt[(q * 8 + 2 * e) * (kTcHD / 2) + lane];
-        const float2 w1 = swt[(q * 8 + 2 * e + 1) * (kTcHD / 2) + lane];
-        const float f0 = bf16lo(uv[e]), f1 = bf16hi(uv[e]);
-        a0 += w0.x * f0 + w1.x * f1;
-        a1 += w0.y * f0 + w1.y * f1;
+        for (int e = 0; e < 8; ++e) {  // e4m3 pairs -> half2 (exact) -> float
+          const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2(
+              (__nv_fp8x2_storage_t)((uv[e >> 1] >> (16 * (e & 1))) & 0xffffu), __NV_E4M3);
+          const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&hr));
+          const float2 w0 = swt[(q * 16 + 2 * e) * (kTcHD / 2) + lane];
+          const float2 w1 = swt[(q * 16 + 2 * e + 1) * (kTcHD / 2) + lane];
+          s0 += w0.x * f.x + w1.x * f.y;
+          s1 += w0.y * f.x + w1.y * f.y;
+        }
+      }
+      a0 += fscale * s0;
+      a1 += fscale * s1;
+    } else {
+      const __nv_bfloat16 *F = static_cast<const __nv_bfloat16 *>(Fv);
+      const uint4 *src = reinterpret_cast<const uint4 *>(F + t * C);
+      for (int q = 0; q < C / 8; ++q) {
+        const uint4 u = __ldg(src + q);  // same address across the warp: one broadcast request
+        const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 w0 = swt[(q * 8 + 2 * e) * (kTcHD / 2) + lane];
+          const float2 w1 = swt[(q * 8 + 2 * e + 1) * (kTcHD / 2) + lane];
+          const float f0 = bf16lo(uv[e]), f1 = bf16hi(uv[e]);
+          a0 += w0.x * f0 + w1.x * f1;
+          a1 += w0.y * f0 + w1.y * f1;
+        }
       }
     }
     const uint32_t pk = (uint32_t)ptx::f32_to_f16(a0) | ((uint32_t)ptx::f32_to_f16(a1) << 16);
@@ -616,19 +641,20 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntex = 3 * P.R * P.R;
   const size_t s0 = (size_t)kTcHD * P.C * 4;
-  cudaError_t e = cudaFuncSetAttribute(preproject_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
+  auto kern = P.tp_fp8 ? preproject_kernel<true> : preproject_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
   if (e != cudaSuccess) return e;
   const float bscale = P.smode != 0 ? 0.0f : (P.agg == 0 ? 1.0f : (1.0f / 3.0f));
-  const __nv_bfloat16 *F = reinterpret_cast<const __nv_bfloat16 *>(P.tp);
+  const uint8_t *F = static_cast<const uint8_t *>(P.tp);
+  const size_t esz = P.tp_fp8 ? 1 : 2;
   const __nv_bfloat16 *W0 = reinterpret_cast<const __nv_bfloat16 *>(P.w[0]);
   const bool cat = P.agg == 2;
   const int nlaunch = cat ? 3 : 1, nt = cat ? P.R * P.R : ntex;
   int g0 = (nt * 32 + 255) / 256;
   if (g0 > sms * 8) g0 = sms * 8;
   for (int pl = 0; pl < nlaunch; ++pl) {
-    preproject_kernel<<<g0, 256, s0, st>>>(F + (size_t)pl * nt * P.C, nt, P.C, cat ? 3 * P.C : P.C,
-                                           W0 + (size_t)pl * P.C, P.b[0], bscale,
+    kern<<<g0, 256, s0, st>>>(F + (size_t)pl * nt * P.C * esz, nt, P.C, cat ? 3 * P.C : P.C,
+                              W0 + (size_t)pl * P.C, P.b[0], bscale, P.tp_scale,
                                            G + (size_t)pl * nt * kTcHD, pl == 0 ? counter : nullptr,
                                            pl == 0 ? G + (size_t)ntex * kTcHD : nullptr);
     e = cudaGetLastError();

@@ -62,6 +62,33 @@ def round_to_bf16(x: np.ndarray) -> np.ndarray:
     return bf16_bits_to_f32(to_bf16_bits(x))
 
 
+def e4m3_values() -> np.ndarray:
+    """The 256 OCP FP8 E4M3 code points as float32 (sign | 4-bit exponent, bias 7 | 3-bit
+    mantissa; exponent 0 is subnormal; S.1111.111 is NaN, no infinities)."""
+    c = np.arange(256)
+    sign = np.where(c & 0x80, -1.0, 1.0)
+    e, m = (c >> 3) & 0xF, c & 7
+    v = np.where(e == 0, m / 8.0 * 2.0 ** -6, (1.0 + m / 8.0) * 2.0 ** (e - 7.0)) * sign
+    v[(c & 0x7F) == 0x7F] = np.nan
+    return v.astype(np.float32)
+
+
+def to_e4m3(x: np.ndarray, scale: float = 1.0):
+    """x / scale rounded to the nearest E4M3 value (ties to the even code), saturating at
+    +-448 -> (codes uint8 [same shape], the stored values scale * e4m3 as float32)."""
+    tab = e4m3_values().astype(np.float64)
+    pos = np.arange(0, 0x7F)  # finite non-negative codes, increasing values
+    y = np.asarray(x, np.float64) / scale
+    a = np.minimum(np.abs(y), tab[0x7E])
+    i = np.clip(np.searchsorted(tab[pos], a), 1, len(pos) - 1)
+    lo, hi = tab[pos[i - 1]], tab[pos[i]]
+    take_hi = (a - lo > hi - a) | ((a - lo == hi - a) & (pos[i] % 2 == 0))
+    code = np.where(take_hi, pos[i], pos[i - 1]).astype(np.uint8)
+    code = np.where((y < 0) & (code != 0), code | 0x80, code).astype(np.uint8)
+    vals = (tab[code] * scale).astype(np.float32)
+    return code.reshape(np.shape(x)), vals.reshape(np.shape(x))
+
+
 # --------------------------------------------------------------------------
 # cameras
 # --------------------------------------------------------------------------

@@ -209,3 +209,50 @@ def test_backward_variants(C, HD, agg, mode):
     for l in range(3):
         assert _close(dW[l].cpu().numpy(), oW[l]), l
         assert _close(db[l].cpu().numpy(), ob[l]), l
+
+
+# ------------------------------------------------------------------ fp8 triplane storage
+def _fp8_setup(scale, C=32, H=12, W=11, N=48):
+    tp = wl.blob_triplane(16, C, seed=2)
+    codes, vals = wl.to_e4m3(tp, scale)
+    m = wl.bf16_mlp(wl.blob_mlp(C, 64, 4, seed=3))
+    cams = _cams(H, W)
+    dev = torch.device("cuda")
+    t8 = torch.from_numpy(codes).to(dev).view(torch.float8_e4m3fn)
+    intr, c2w = dev_cams(cams)
+    return vals, m, cams, t8, intr, c2w, api.DeviceMLP.from_host(m, "bf16", dev)
+
+
+@pytest.mark.parametrize("scale", [1.0, 0.375])
+def test_fp8_triplane_render_tc(scale):
+    """Row f4: E4M3 triplane storage (value = scale * e4m3) on the tensor-core engine
+    equals the oracle rendering the dequantised values, at the bf16 TC bar."""
+    vals, m, cams, t8, intr, c2w, mlp = _fp8_setup(scale)
+    H, W = cams.height, cams.width
+    rgb, alpha = api.dmv3d_render_views(t8, intr, c2w, H, W, mlp, samples_per_ray=48,
+                                        engine="tcgen05", fp8_scale=scale)
+    orgb, oalpha = oracle.render_views(vals, cams, m, 48)
+    assert np.max(np.abs(rgb.cpu().numpy() - orgb)) < RGB_TOL
+    assert np.max(np.abs(alpha.cpu().numpy() - oalpha)) < ALPHA_TOL
+
+
+def test_fp8_triplane_backward_tc():
+    vals, m, cams, t8, intr, c2w, mlp = _fp8_setup(0.5)
+    H, W = cams.height, cams.width
+    rng = np.random.default_rng(5)
+    g = rng.normal(size=(cams.num_views, 3, H, W)).astype(np.float32)
+    dF, dW, db = api.dmv3d_render_backward(t8, intr, c2w, H, W, mlp, torch.from_numpy(g).cuda(),
+                                           samples_per_ray=48, engine="tcgen05", fp8_scale=0.5)
+    oF, oW, ob = oracle.render_backward(vals, cams, m, 48, g)
+    rel = lambda a, b: np.max(np.abs(a - b)) / np.max(np.abs(b))  # noqa: E731
+    assert rel(dF.cpu().numpy(), oF) < 2e-2
+    for l in range(4):
+        assert rel(dW[l].cpu().numpy(), oW[l]) < 2e-2 and rel(db[l].cpu().numpy(), ob[l]) < 2e-2
+
+
+def test_fp8_triplane_needs_tc_engine():
+    _, _, cams, t8, intr, c2w, mlp = _fp8_setup(1.0)
+    with pytest.raises(api._abi.DMV3DError) as e:
+        api.dmv3d_render_views(t8, intr, c2w, cams.height, cams.width, mlp, samples_per_ray=8,
+                               engine="simt")
+    assert e.value.status == 2  # UNSUPPORTED
