@@ -102,13 +102,17 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
                : "memory");
   return v;
 }
-// dz = dh where h > 0 (fp16 h, fp32 dh), packed fp16
+// dz = dh where h > 0 (fp16 h, fp32 dh), packed fp16: one cvt, one HSET2, one LOP
 __device__ __forceinline__ uint32_t mask_pack(uint32_t h2, float d0, float d1) {
   const __half2 h = *reinterpret_cast<const __half2 *>(&h2);
-  const float a = __low2float(h) > 0.0f ? d0 : 0.0f;
-  const float b = __high2float(h) > 0.0f ? d1 : 0.0f;
-  return ptx::pack_f16x2(a, b);
+  return ptx::pack_f16x2(d0, d1) & __hgt2_mask(h, __float2half2_rn(0.0f));
 }
+
+// the forward tensor-core engine's head activations (fast exp / divide)
+__device__ __forceinline__ float softplus_fast(float x) {
+  return __logf(1.0f + __expf(-fabsf(x))) + fmaxf(x, 0.0f);
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 }  // namespace
 
@@ -118,7 +122,8 @@ size_t tc_backward_workspace_bytes(int R, int HD) {
 }
 
 bool tc_backward_supported(int C, int HD, int L) {
-  return tc_supported(C, HD, L) && bw_smem_bytes<1>(L) <= kSmemLimit;
+  return tc_supported(C, HD, L) && bw_smem_bytes<1>(L) <= kSmemLimit &&
+         kHD + (L - 2) * kHD + 16 <= 512;
 }
 
 template <int NG>
@@ -182,11 +187,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = sh->tmem_base + (uint32_t)(g * kHD);
-  const uint32_t tmem_dw = sh->tmem_base + (uint32_t)(NG * kHD);
+  // TMEM per group: the accumulator (z / dh / dG) and the group's own dW^T accumulators
+  // (not shared between groups: accumulating into one region would chain the groups' MMAs)
+  const uint32_t tmem = sh->tmem_base + (uint32_t)g * (kHD + ndw);
+  const uint32_t tmem_dw = tmem + (uint32_t)kHD;
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tmem_row = tmem + lane_off;
-  if (g == 0) {  // zero the shared dW accumulators (group 0's warps cover the 128 lanes)
+  {  // zero this group's dW accumulators (its 4 warps cover the 128 lanes)
     const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     for (uint32_t c = 0; c < ndw; c += 16) ptx::tmem_st16(tmem_dw + lane_off + c, z);
     ptx::tmem_st_wait();
@@ -450,9 +457,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
       forward(k0, o);
       float sigma = 0.0f, c[3] = {0.f, 0.f, 0.f};
       if (sv) {
-        sigma = softplus_f(o[0] + P.dshift);
+        sigma = softplus_fast(o[0] + P.dshift);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) c[e] = sigmoid_f(o[1 + e]) * (1.0f + 2.0f * P.weps) - P.weps;
+        for (int e = 0; e < 3; ++e) c[e] = sigmoid_fast(o[1 + e]) * (1.0f + 2.0f * P.weps) - P.weps;
       }
       const float tau = sv ? sigma * delta : 0.0f;
       float S = tau;
@@ -461,10 +468,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
         const float y = __shfl_up_sync(0xffffffffu, S, s, kChunk);
         if (q >= s) S += y;
       }
-      const float w = T * expf(-(S - tau)) * (-expm1f(-tau));
+      const float w = T * __expf(-(S - tau)) * (-expm1f(-tau));
 #pragma unroll
       for (int e = 0; e < 3; ++e) acc[e] += w * c[e];
-      T *= expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
+      T *= __expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
     }
     float Ctot[3];
 #pragma unroll
@@ -485,10 +492,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
       float sigma = 0.0f, zs = 0.0f, c[3] = {0.f, 0.f, 0.f}, sg[3] = {0.f, 0.f, 0.f};
       if (sv) {
         zs = o[0] + P.dshift;
-        sigma = softplus_f(zs);
+        sigma = softplus_fast(zs);
 #pragma unroll
         for (int e = 0; e < 3; ++e) {
-          sg[e] = sigmoid_f(o[1 + e]);
+          sg[e] = sigmoid_fast(o[1 + e]);
           c[e] = sg[e] * (1.0f + 2.0f * P.weps) - P.weps;
         }
       }
@@ -499,9 +506,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
         const float y = __shfl_up_sync(0xffffffffu, S, s, kChunk);
         if (q >= s) S += y;
       }
-      const float Tk = T * expf(-(S - tau));
+      const float Tk = T * __expf(-(S - tau));
       const float w = Tk * (-expm1f(-tau));
-      const float Tk1 = Tk * expf(-tau);
+      const float Tk1 = Tk * __expf(-tau);
       float dtau = gA * TN;
 #pragma unroll
       for (int e = 0; e < 3; ++e) {
@@ -514,11 +521,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
         dtau += gr[e] * (Tk1 * c[e] - (Ctot[e] - (Pc[e] + sc)));
         Pc[e] += __shfl_sync(0xffffffffu, sc, kChunk - 1, kChunk);
       }
-      T *= expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
+      T *= __expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
       float d4[4] = {0.f, 0.f, 0.f, 0.f};
       if (sv) {
         const float cs = w * (1.0f + 2.0f * P.weps);
-        d4[0] = dtau * delta * sigmoid_f(zs);
+        d4[0] = dtau * delta * sigmoid_fast(zs);
 #pragma unroll
         for (int e = 0; e < 3; ++e) d4[1 + e] = gr[e] * cs * sg[e] * (1.0f - sg[e]);
       }
@@ -561,15 +568,18 @@ __global__ void __launch_bounds__(128 * NG, 1)
         if (tid == 0) {
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
-          // dh_l = dz_l W_l: A = dz_l (K-major, K = 64 outputs), B = W_l as [out][in] MN-major
-          for (int ks = 0; ks < kHD / 16; ++ks)
-            ptx::mma_f16_ss(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
-                            ptx::smem_desc(wbase + ks * 2 * kWSbo, kWSbo, 128, 0), id_dh, ks > 0 ? 1u : 0u);
-          // [h_l | 1]^T dz_l -> dW_l^T (rows 0..63), db_l (row 64); K = the 128 samples
+          // dh_l = dz_l W_l: A = dz_l (K-major, K = 64 outputs), B = W_l as [out][in] MN-major;
+          // [h_l | 1]^T dz_l -> dW_l^T (rows 0..63), db_l (row 64), K = the 128 samples.
+          // The two accumulation chains are issued interleaved: the tensor pipe overlaps
+          // independent chains but runs one chain's dependent K-steps back to back.
           const uint32_t dcol = tmem_dw + (uint32_t)((l - 1) * kHD);
-          for (int ks = 0; ks < 8; ++ks)
+          for (int ks = 0; ks < 8; ++ks) {
+            if (ks < kHD / 16)
+              ptx::mma_f16_ss(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
+                              ptx::smem_desc(wbase + ks * 2 * kWSbo, kWSbo, 128, 0), id_dh, ks > 0 ? 1u : 0u);
             ptx::mma_f16_ss(dcol, ptx::smem_desc(hT(l) + ks * 2 * kHSbo, kHSbo, 128, 0),
                             ptx::smem_desc(ht + ks * 2 * kHSbo, kHSbo, 128, 0), id_dw, 1u);
+          }
           ptx::mma_commit(&sh->mbar[g]);
         }
         mma_wait();
@@ -618,7 +628,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (g == 0) {
+  {
     const int f = tid;  // TMEM lane = input feature (64 = the bias row)
     for (int l = 1; l < L; ++l) {
       const bool head = l == L - 1;
@@ -776,8 +786,8 @@ cudaError_t launch_render_backward_tc(const RenderParams &P0, const GradParams &
   const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
   const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
   timer_begin(P.timer, st);
-  e = bw_smem_bytes<2>(P.L) <= kSmemLimit ? launch_bwd_k1<2>(P, Gp, dG, sms, npatch, st)
-                                          : launch_bwd_k1<1>(P, Gp, dG, sms, npatch, st);
+  const bool ng2 = bw_smem_bytes<2>(P.L) <= kSmemLimit && 2 * (kHD + (P.L - 2) * kHD + 16) <= 512;
+  e = ng2 ? launch_bwd_k1<2>(P, Gp, dG, sms, npatch, st) : launch_bwd_k1<1>(P, Gp, dG, sms, npatch, st);
   timer_end(P.timer, st);
   if (e != cudaSuccess) return e;
   // K2: dF = dG W0 (per plane block for concat); K3: dW0, db0
