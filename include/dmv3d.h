@@ -147,6 +147,13 @@ typedef struct {
                               alpha and x_prev.  The arrays may be NULL when unused.  */
   float *const *peer_alpha;
   float *const *peer_x_prev;
+  int32_t tile_size;       /* interleaved ray tiles, render / DDIM calls:
+                              0 = off; else T > 0 (a multiple of 4) and only the pixels
+                              of tiles tau = (v ceil(H/T) + i/T) ceil(W/T) + j/T with
+                              tau mod tile_count == tile_rank are rendered and written
+                              (the others are left untouched).  Balances AABB misses and
+                              early termination across ranks.                          */
+  int32_t tile_rank, tile_count;
   const float *fwd_rgb;    /* backward only, optional DEVICE [V][3][H][W] / [V][H][W]: the  */
   const float *fwd_alpha;  /* forward render of the same call (rgb, alpha; term_eps 0, or
                               within term_eps).  Given both, the backward takes C = rgb

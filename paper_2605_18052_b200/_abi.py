@@ -55,7 +55,8 @@ class RenderOpts(ct.Structure):
                 ("workspace_bytes", ct.c_uint64), ("timer", ct.c_void_p),
                 ("plucker", ct.c_void_p), ("num_peers", ct.c_int32),
                 ("peer_rgb", ct.c_void_p), ("peer_alpha", ct.c_void_p),
-                ("peer_x_prev", ct.c_void_p), ("fwd_rgb", ct.c_void_p), ("fwd_alpha", ct.c_void_p)]
+                ("peer_x_prev", ct.c_void_p), ("tile_size", ct.c_int32), ("tile_rank", ct.c_int32),
+                ("tile_count", ct.c_int32), ("fwd_rgb", ct.c_void_p), ("fwd_alpha", ct.c_void_p)]
 
 
 class DdimParams(ct.Structure):

@@ -78,10 +78,11 @@ def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, wid
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
                 term_eps=0.0, ray_range=None, engine="auto", counters=None, workspace=None,
-                timer=None, plucker=None, peers=None, fwd=None):
+                timer=None, plucker=None, peers=None, fwd=None, tiles=None):
     """`peers`: optional dict with "rgb" / "alpha" / "x_prev" lists of device addresses
     (ints, 0 = skip) laid out like the corresponding outputs (P2P copies, see the ABI).
-    `fwd`: (rgb, alpha) of the forward render, for the backward (opts.fwd_rgb / fwd_alpha)."""
+    `fwd`: (rgb, alpha) of the forward render, for the backward (opts.fwd_rgb / fwd_alpha).
+    `tiles`: (tile_size, rank, count): interleaved ray tiles, only this rank's are rendered."""
     b, e = (-1, -1) if ray_range is None else ray_range
     ws_ptr = None if workspace is None else workspace.data_ptr()
     ws_len = 0 if workspace is None else workspace.numel() * workspace.element_size()
@@ -92,6 +93,8 @@ def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 
                         None if plucker is None else plucker.data_ptr())
     if fwd is not None:
         o.fwd_rgb, o.fwd_alpha = fwd[0].data_ptr(), fwd[1].data_ptr()
+    if tiles is not None:
+        o.tile_size, o.tile_rank, o.tile_count = (int(x) for x in tiles)
     if peers:
         n = max(len(peers.get(k) or []) for k in ("rgb", "alpha", "x_prev"))
         arrs = {}

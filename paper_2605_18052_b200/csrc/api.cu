@@ -139,6 +139,9 @@ dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
   if (o->workspace && (reinterpret_cast<uintptr_t>(o->workspace) & 255u))
     return fail(DMV3D_ERR_ALIGNMENT, "opts.workspace is not 256-byte aligned");
   CHECK_ARG(o->num_peers >= 0 && o->num_peers <= kMaxPeers, "opts: num_peers must be in [0, 7]");
+  CHECK_ARG(o->tile_size == 0 || (o->tile_size > 0 && o->tile_size % 4 == 0 && o->tile_count >= 1 &&
+                                  o->tile_rank >= 0 && o->tile_rank < o->tile_count),
+            "opts: tiles need tile_size % 4 == 0 and 0 <= tile_rank < tile_count");
   return DMV3D_OK;
 }
 
@@ -193,6 +196,9 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.timer = o->timer;
     P.plucker = o->plucker;
     P.npeers = o->num_peers;
+    P.tile_size = o->tile_size;
+    P.tile_rank = o->tile_rank;
+    P.tile_count = o->tile_count > 0 ? o->tile_count : 1;
     for (int k = 0; k < o->num_peers; ++k) {
       P.peer_rgb[k] = o->peer_rgb ? o->peer_rgb[k] : nullptr;
       P.peer_alpha[k] = o->peer_alpha ? o->peer_alpha[k] : nullptr;
@@ -373,6 +379,8 @@ dmv3d_status dmv3d_render_backward(const dmv3d_triplane *triplane, const dmv3d_c
     return s;
   if ((s = check_mlp(mlp, triplane, opts->agg)) != DMV3D_OK) return s;
   CHECK_ARG(grad_rgb && grad_triplane && grad_weights && grad_biases, "backward: NULL gradient buffer");
+  if (opts->tile_size)
+    return fail(DMV3D_ERR_UNSUPPORTED, "backward: interleaved tiles are a render option (use ray ranges)");
   CHECK_ALIGN(grad_rgb, "grad_rgb");
   if (grad_alpha) CHECK_ALIGN(grad_alpha, "grad_alpha");
   CHECK_ALIGN(grad_triplane, "grad_triplane");

@@ -66,10 +66,27 @@ struct RenderParams {
   // out like rgb / alpha / x_prev
   int32_t npeers;
   float *peer_rgb[kMaxPeers], *peer_alpha[kMaxPeers], *peer_xp[kMaxPeers];
+  // interleaved ray tiles: tile_size > 0 keeps only the pixels of tiles
+  // tau = (v ceil(H/T) + i/T) ceil(W/T) + j/T with tau mod tile_count == tile_rank
+  int32_t tile_size, tile_rank, tile_count;
   // density grid mode of the tensor-core engine (row f3): G^3 points, x fastest
   int32_t grid_res;
   float *grid_sigma, *grid_rgb;
 };
+
+// ---------------------------------------------------------------- ray tiles (§8e)
+__host__ __device__ inline int64_t tile_of(int v, int i, int j, int H, int W, int T) {
+  const int64_t th = (H + T - 1) / T, tw = (W + T - 1) / T;
+  return ((int64_t)v * th + i / T) * tw + j / T;
+}
+// tiles of views [v_lo, v_hi] owned by `rank`: the first id and how many
+__host__ __device__ inline void owned_tiles(int v_lo, int v_hi, int H, int W, int T, int rank,
+                                            int count, int64_t &first, int64_t &n) {
+  const int64_t per_view = (int64_t)((H + T - 1) / T) * ((W + T - 1) / T);
+  const int64_t t0 = (int64_t)v_lo * per_view, t1 = (int64_t)(v_hi + 1) * per_view;
+  first = t0 + (((int64_t)rank - t0) % count + count) % count;
+  n = first < t1 ? (t1 - first + count - 1) / count : 0;
+}
 
 // ---------------------------------------------------------------- a1: rays
 // Pinhole camera, pixel centre at +1/2, OpenCV axes, unit direction.

@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(kSimtThreads)
   for (int64_t r = P.ray_begin + warp0; r < P.ray_end; r += nwarps) {
     int v, i, j;
     ray_pixel(r, P.H, P.W, v, i, j);
+    if (P.tile_size > 0 && tile_of(v, i, j, P.H, P.W, P.tile_size) % P.tile_count != P.tile_rank)
+      continue;  // another rank's tile
     const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
     if (P.plucker && lane < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, lane, ray);
     n_rays++;

@@ -265,8 +265,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int v_hi = (int)((P.ray_end - 1) / HW);
   const int PH = (P.H + kPatch - 1) / kPatch, PW = (P.W + kPatch - 1) / kPatch;
   const int GB[3] = {(P.grid_res + 7) / 8, (P.grid_res + 3) / 4, (P.grid_res + 3) / 4};
+  // interleaved ray tiles (§8e): the work queue enumerates this rank's tiles' patches
+  const int TP = P.tile_size / kPatch;  // patches per tile side (0: no tiling)
+  int64_t tile_first = 0, tile_n = 0;
+  if (!GRID && TP > 0)
+    owned_tiles(v_lo, v_hi, P.H, P.W, P.tile_size, P.tile_rank, P.tile_count, tile_first, tile_n);
+  const int64_t TH = TP > 0 ? (P.H + P.tile_size - 1) / P.tile_size : 1;
+  const int64_t TW = TP > 0 ? (P.W + P.tile_size - 1) / P.tile_size : 1;
   const int64_t npatch = GRID ? (int64_t)GB[0] * GB[1] * GB[2]
-                              : (int64_t)(v_hi - v_lo + 1) * PH * PW;
+                              : TP > 0 ? tile_n * TP * TP : (int64_t)(v_hi - v_lo + 1) * PH * PW;
   const int slot = tid >> 3, q = tid & 7;
   const int R = P.R;
   const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
@@ -361,10 +368,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       ray.hit = pix;
     } else {
-      v = v_lo + (int)(patch / ((int64_t)PH * PW));
-      const int prem = (int)(patch % ((int64_t)PH * PW));
-      i = (prem / PW) * kPatch + (slot >> 2);
-      j = (prem % PW) * kPatch + (slot & 3);
+      int prow, pcol;
+      if (TP > 0) {  // k-th owned tile, w-th patch in it
+        const int64_t tau = tile_first + (patch / (TP * TP)) * P.tile_count;
+        const int w = (int)(patch % (TP * TP));
+        v = (int)(tau / (TH * TW));
+        const int64_t trem = tau % (TH * TW);
+        prow = (int)(trem / TW) * TP + w / TP;
+        pcol = (int)(trem % TW) * TP + w % TP;
+      } else {
+        v = v_lo + (int)(patch / ((int64_t)PH * PW));
+        const int prem = (int)(patch % ((int64_t)PH * PW));
+        prow = prem / PW;
+        pcol = prem % PW;
+      }
+      i = prow * kPatch + (slot >> 2);
+      j = pcol * kPatch + (slot & 3);
       r = (int64_t)v * HW + (int64_t)i * P.W + j;
       pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
       if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
@@ -686,8 +705,17 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
     e = ng4 ? launch_k1<4, true>(P, sms, nb, st) : launch_k1<2, true>(P, sms, nb, st);
   } else {
     const int64_t HW = (int64_t)P.H * P.W;
-    const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
-    const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
+    const int v_lo = (int)(P.ray_begin / HW), v_hi = (int)((P.ray_end - 1) / HW);
+    int64_t npatch = (int64_t)(v_hi - v_lo + 1) * ((P.H + 3) / 4) * ((P.W + 3) / 4);
+    if (P.tile_size > 0) {
+      int64_t first = 0, n = 0;
+      owned_tiles(v_lo, v_hi, P.H, P.W, P.tile_size, P.tile_rank, P.tile_count, first, n);
+      npatch = n * (P.tile_size / 4) * (P.tile_size / 4);
+      if (npatch == 0) {
+        timer_end(P.timer, st);
+        return cudaSuccess;
+      }
+    }
     e = ng4 ? launch_k1<4, false>(P, sms, npatch, st) : launch_k1<2, false>(P, sms, npatch, st);
   }
   timer_end(P.timer, st);

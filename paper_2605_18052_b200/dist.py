@@ -19,6 +19,12 @@ independent.  Two partitions are provided, in the priority order of §8e:
   itself stores every value into all peers' buffers over NVLink (opts.peers of the
   ABI); one device-side barrier replaces the three all-gathers.
 
+* interleaved ray tiles (`denoise_step_tile_sharded`): every rank renders the
+  T x T pixel tiles tau = (v ceil(H/T) + i/T) ceil(W/T) + j/T with tau mod P == rank
+  of every view (opts.tile_* of the ABI), which spreads AABB misses and early-
+  terminated rays evenly; each rank's outputs start at zero, so one all-reduce (sum)
+  of the three outputs assembles them (every pixel has exactly one non-zero writer).
+
 The render call is injectable (`render_fn`) so the shard/merge logic is
 tested on CPU with gloo and the CPU oracle (tests/test_dist_gloo.py); the
 default is libdmv3d's fused step.  The P2P path needs GPUs with peer access; its
@@ -156,6 +162,39 @@ def _denoise_step_view_sharded_p2p(triplane, intrinsics, c2w, height, width, mlp
     # every rank's peer stores have landed once all ranks pass the device-side barrier
     ha.barrier()
     return xp[:ddim_views], rgb, alpha
+
+
+def tile_owner(v: int, i: int, j: int, height: int, width: int, tile: int, world: int) -> int:
+    """Rank that renders pixel (v, i, j) under the interleaved-tile split."""
+    th, tw = -(-height // tile), -(-width // tile)
+    return ((v * th + i // tile) * tw + j // tile) % world
+
+
+def denoise_step_tile_sharded(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
+                              x_t, ddim_views: int, group=None, src: int = 0,
+                              broadcast_triplane: bool = True, render_fn=None, tile: int = 16,
+                              **opts):
+    """One denoising step of one asset, T x T ray tiles dealt round robin to the ranks.
+    Returns the full (x_prev, rgb, alpha) on every rank."""
+    render_fn = render_fn or default_render_fn
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    V = int(c2w.shape[0])
+    dev = triplane.device
+    if broadcast_triplane and world > 1:
+        dist.broadcast(triplane, src=src, group=group)
+    HW = height * width
+    n_x, n_rgb = ddim_views * 3 * HW, V * 3 * HW
+    flat = torch.zeros(n_x + n_rgb + V * HW, device=dev, dtype=torch.float32)  # one collective
+    xp = flat[:n_x].view(ddim_views, 3, height, width)
+    rgb = flat[n_x:n_x + n_rgb].view(V, 3, height, width)
+    alpha = flat[n_x + n_rgb:].view(V, height, width)
+    render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
+              x_t if ddim_views else None, xp if ddim_views else None, rgb, alpha,
+              tiles=(tile, rank, world), **opts)
+    if world > 1:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return xp, rgb, alpha
 
 
 def max_over_ranks(value: float, device, group=None) -> float:

@@ -72,6 +72,10 @@ def _valid_structs(keep):
     (lambda t, c, m, o: setattr(o, "engine", _abi.ENGINE_TCGEN05), _abi.ERR_UNSUPPORTED),
     (lambda t, c, m, o: setattr(m, "hidden", 17), _abi.ERR_UNSUPPORTED),
     (lambda t, c, m, o: setattr(t, "sample_mode", 2), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: setattr(t, "dtype", 3), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: (setattr(o, "tile_size", 6), setattr(o, "tile_count", 2)), _abi.ERR_INVALID_ARG),
+    (lambda t, c, m, o: (setattr(o, "tile_size", 16), setattr(o, "tile_rank", 2),
+                         setattr(o, "tile_count", 2)), _abi.ERR_INVALID_ARG),
     (lambda t, c, m, o: setattr(o, "agg", 3), _abi.ERR_INVALID_ARG),
     (lambda t, c, m, o: setattr(o, "agg", _abi.AGG_CONCAT), _abi.ERR_INVALID_ARG),  # in_dim != 3C
     (lambda t, c, m, o: (setattr(o, "agg", _abi.AGG_CONCAT), setattr(m, "in_dim", 24),

@@ -43,6 +43,68 @@ def _oracle_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t_prev
         x_prev.copy_(torch.from_numpy(xp.astype(np.float32)))
 
 
+def _oracle_tile_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t_prev, x_t, x_prev,
+                           rgb, alpha, tiles, samples_per_ray=16):
+    """The oracle as a tile-sharded renderer: writes only the pixels of this rank's tiles
+    (ownership from the tile formula written out here, independently of dist.py)."""
+    T, rank, world = tiles
+    full_rgb, full_a = torch.zeros_like(rgb), torch.zeros_like(alpha)
+    full_x = torch.zeros_like(x_prev) if x_prev is not None else None
+    _oracle_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t_prev, x_t, full_x,
+                      full_rgb, full_a, samples_per_ray)
+    V = rgb.shape[0]
+    th, tw = -(-H // T), -(-W // T)
+    for v in range(V):
+        for i in range(H):
+            for j in range(W):
+                if ((v * th + i // T) * tw + j // T) % world == rank:
+                    rgb[v, :, i, j] = full_rgb[v, :, i, j]
+                    alpha[v, i, j] = full_a[v, i, j]
+                    if x_prev is not None and v < x_prev.shape[0]:
+                        x_prev[v, :, i, j] = full_x[v, :, i, j]
+
+
+def _tile_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tp, m, cams = _workload()
+        triplane = torch.from_numpy(tp) if rank == 0 else torch.zeros_like(torch.from_numpy(tp))
+        x_t = torch.from_numpy(wl.gaussian((3, 3, 6, 5), 4))
+        xp, rgb, alpha = pdist.denoise_step_tile_sharded(
+            triplane, torch.from_numpy(cams.intrinsics), torch.from_numpy(cams.c2w), 6, 5, m,
+            schedule.cosine_alpha_bar(), 980, 960, x_t, ddim_views=3,
+            render_fn=_oracle_tile_render_fn, tile=4, samples_per_ray=16)
+        np.savez(os.path.join(out_dir, f"t{rank}.npz"), xp=xp.numpy(), rgb=rgb.numpy(),
+                 alpha=alpha.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tile_sharded_step_matches_single_process(tmp_path):
+    world = 2
+    mp.spawn(_tile_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    import oracle
+    tp, m, cams = _workload()
+    orgb, oalpha = oracle.render_views(tp, cams, m, 16, threads=1)
+    oxp = oracle.ddim_step(schedule.cosine_alpha_bar(), 980, 960, wl.gaussian((3, 3, 6, 5), 4), orgb[:3])
+    for r in range(world):
+        d = np.load(tmp_path / f"t{r}.npz")
+        assert np.array_equal(d["rgb"], orgb.astype(np.float32))
+        assert np.array_equal(d["alpha"], oalpha.astype(np.float32))
+        assert np.array_equal(d["xp"], oxp.astype(np.float32))
+
+
+@pytest.mark.parametrize("H,W,T,P", [(6, 5, 4, 2), (16, 16, 4, 3), (33, 20, 8, 4)])
+def test_tile_owner_partition(H, W, T, P):
+    """Every pixel has one owner; owners cycle over consecutive tiles."""
+    owners = np.array([[[pdist.tile_owner(v, i, j, H, W, T, P) for j in range(W)] for i in range(H)]
+                       for v in range(3)])
+    assert owners.min() >= 0 and owners.max() < P
+    assert owners[0, 0, 0] == 0 and (W > T) == (owners[0, 0, min(T, W - 1)] == 1 % P)
+
+
 def _worker(rank, world, port, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

@@ -167,3 +167,41 @@ def test_peer_stores_write_every_copy(engine, dtype):
     api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=24, engine=engine,
                            ray_range=(2 * H * W, 4 * H * W), peers={"rgb": [pr.data_ptr()]})
     assert torch.equal(pr[2:], rgb[2:]) and (pr[:2] == -1.0).all()
+
+
+@pytest.mark.parametrize("engine,dtype,T,P", [("tcgen05", "bf16", 16, 3), ("tcgen05", "bf16", 8, 2),
+                                              ("simt", "f32", 16, 3)])
+def test_interleaved_tiles_union_is_the_full_step(engine, dtype, T, P):
+    """SURVEY §8e interleaved ray tiles: rank r writes exactly the pixels of tiles
+    tau = r mod P (others untouched), and the union over ranks is the one-GPU step
+    bitwise (tiles are whole 4x4 patches, so the TC tile footprint is unchanged)."""
+    from paper_2605_18052_b200 import dist as pdist
+    from paper_2605_18052_b200 import schedule
+    tp = wl.blob_triplane(12, 32, seed=2)
+    m = wl.blob_mlp(32, 64, 4, seed=3)
+    if dtype == "bf16":
+        tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
+    H, W = 37, 29
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 2), wl.novel_cameras(H, W, 2, seed=4))
+    t, intr, c2w, mlp = dev_workload(wl.Workload("tiles", tp, cams, m, 24, dtype))
+    ab = schedule.cosine_alpha_bar()
+    x_t = torch.from_numpy(wl.gaussian((2, 3, H, W), 4)).cuda()
+    xp, rgb, alpha = api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, ab, 980, 960, x_t,
+                                                samples_per_ray=24, engine=engine, term_eps=1e-4)
+    owner = torch.tensor([[[pdist.tile_owner(v, i, j, H, W, T, P) for j in range(W)]
+                           for i in range(H)] for v in range(4)], device="cuda")
+    u_xp, u_rgb, u_a = torch.zeros_like(xp), torch.zeros_like(rgb), torch.zeros_like(alpha)
+    for r in range(P):
+        sx = torch.full_like(xp, float("nan"))
+        sr = torch.full_like(rgb, float("nan"))
+        sa = torch.full_like(alpha, float("nan"))
+        api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, ab, 980, 960, x_t, x_prev=sx, rgb=sr,
+                                   alpha=sa, samples_per_ray=24, engine=engine, term_eps=1e-4,
+                                   tiles=(T, r, P))
+        mine = owner == r
+        assert not torch.isnan(sa[mine]).any() and torch.isnan(sa[~mine]).all()
+        u_a[mine] = sa[mine]
+        u_rgb[mine.unsqueeze(1).expand_as(rgb)] = sr[mine.unsqueeze(1).expand_as(rgb)]
+        m2 = mine[:2].unsqueeze(1).expand_as(xp)
+        u_xp[m2] = sx[m2]
+    assert torch.equal(u_a, alpha) and torch.equal(u_rgb, rgb) and torch.equal(u_xp, xp)
