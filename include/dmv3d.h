@@ -265,9 +265,12 @@ dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp 
 /* ------------------------------------------------------ host-buffer variant */
 /* Same step with every tensor pointer (triplane data, weights, biases,
  * intrinsics, c2w, x_t, z, x_prev, rgb, alpha) a HOST pointer (pinned for
- * async copies).  The workspace owns grow-only device buffers; one
- * workspace per thread/stream.  Copies in, launches, copies out, all on
- * `stream`; the host buffers are valid after the stream is synchronised. */
+ * async copies).  The workspace owns grow-only device buffers, a copy stream and
+ * events; one workspace per thread/stream.  Copies in on `stream`, then the views
+ * are rendered in up to 4 view chunks (ray ranges; bitwise the same result as one
+ * launch) and each chunk's outputs are copied out on the workspace's copy stream
+ * while the next chunk renders; `stream` waits for the last copy, so the host
+ * buffers are valid after `stream` is synchronised. */
 typedef struct dmv3d_workspace dmv3d_workspace;
 dmv3d_status dmv3d_workspace_create(dmv3d_workspace **ws);
 dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws);

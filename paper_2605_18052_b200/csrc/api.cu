@@ -279,7 +279,7 @@ dmv3d_status cuda_status(cudaError_t e, const char *what) {
 dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const dmv3d_mlp *m,
                          const dmv3d_render_opts *o, const dmv3d_ddim_params *d, const float *x_t,
                          const float *z, float *x_prev, float *rgb, float *alpha,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool reuse_g = false) {
   dmv3d_status s;
   if ((s = check_cams(c)) != DMV3D_OK) return s;
   if ((s = check_triplane(t)) != DMV3D_OK) return s;
@@ -292,6 +292,7 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
   fill_common(P, t, c, m, o);
   P.rgb = rgb;
   P.alpha = alpha;
+  P.reuse_g = reuse_g ? 1 : 0;
   if (d) {
     CHECK_ARG(d->ddim_views >= 1 && d->ddim_views <= c->num_views, "ddim: need 1 <= ddim_views <= V");
     if (d->ddim_views > 64) return fail(DMV3D_ERR_UNSUPPORTED, "ddim: at most 64 DDIM views per call");
@@ -688,6 +689,11 @@ struct dmv3d_workspace {
     size_t cap = 0;
   };
   Buf tp, intr, c2w, xt, z, xp, rgb, alpha, scratch, w[kMaxLayers], b[kMaxLayers];
+  // copy-out pipeline: a stream for device->host copies and one event per view chunk
+  static constexpr int kChunks = 4;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev[kChunks + 1] = {};
+  int dev = -1;
 };
 
 static cudaError_t ws_reserve(dmv3d_workspace::Buf &b, size_t bytes) {
@@ -717,6 +723,10 @@ dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws) {
   for (int l = 0; l < kMaxLayers; ++l) {
     if (ws->w[l].p) cudaFree(ws->w[l].p);
     if (ws->b[l].p) cudaFree(ws->b[l].p);
+  }
+  if (ws->copy) {
+    cudaStreamDestroy(ws->copy);
+    for (auto &ev : ws->ev) cudaEventDestroy(ev);
   }
   delete ws;
   return DMV3D_OK;
@@ -791,15 +801,53 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
       o.workspace_bytes = need;
     }
   }
-  dmv3d_status s = render_impl(&t, &c, &m, &o, ddim, static_cast<const float *>(ws->xt.p),
-                               z ? static_cast<const float *>(ws->z.p) : nullptr,
-                               static_cast<float *>(ws->xp.p),
-                               rgb ? static_cast<float *>(ws->rgb.p) : nullptr,
-                               alpha ? static_cast<float *>(ws->alpha.p) : nullptr, st);
-  if (s != DMV3D_OK) return s;
-  TRY(cudaMemcpyAsync(x_prev, ws->xp.p, img_in, cudaMemcpyDeviceToHost, st));
-  if (rgb) TRY(cudaMemcpyAsync(rgb, ws->rgb.p, V * 3 * HW * 4, cudaMemcpyDeviceToHost, st));
-  if (alpha) TRY(cudaMemcpyAsync(alpha, ws->alpha.p, V * HW * 4, cudaMemcpyDeviceToHost, st));
+  // Render in view chunks (ray ranges on view boundaries: the same patches, hence the same
+  // bits as one launch); each chunk's outputs are copied back on the copy stream while the
+  // next chunk renders.  The projected triplane G is computed by the first launch only.
+  int cur_dev = 0;
+  TRY(cudaGetDevice(&cur_dev));
+  if (ws->copy == nullptr || ws->dev != cur_dev) {
+    if (ws->copy) {
+      cudaStreamDestroy(ws->copy);
+      for (auto &ev : ws->ev) cudaEventDestroy(ev);
+    }
+    TRY(cudaStreamCreateWithFlags(&ws->copy, cudaStreamNonBlocking));
+    for (auto &ev : ws->ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ws->dev = cur_dev;
+  }
+  const int nc = (int)(V < (size_t)dmv3d_workspace::kChunks ? V : (size_t)dmv3d_workspace::kChunks);
+  const size_t vpc = (V + nc - 1) / nc;
+  const size_t dv = (size_t)ddim->ddim_views;
+  const bool tc = o.workspace != nullptr && o.engine != DMV3D_ENGINE_SIMT;
+  for (int k = 0; k < nc; ++k) {
+    const size_t v0 = k * vpc, v1 = (v0 + vpc < V) ? v0 + vpc : V;
+    if (v0 >= v1) break;
+    dmv3d_render_opts ok = o;
+    ok.ray_begin = (int64_t)(v0 * HW);
+    ok.ray_end = (int64_t)(v1 * HW);
+    const dmv3d_status s = render_impl(&t, &c, &m, &ok, ddim, static_cast<const float *>(ws->xt.p),
+                                       z ? static_cast<const float *>(ws->z.p) : nullptr,
+                                       static_cast<float *>(ws->xp.p),
+                                       rgb ? static_cast<float *>(ws->rgb.p) : nullptr,
+                                       alpha ? static_cast<float *>(ws->alpha.p) : nullptr, st,
+                                       tc && k > 0);
+    if (s != DMV3D_OK) return s;
+    TRY(cudaEventRecord(ws->ev[k], st));
+    TRY(cudaStreamWaitEvent(ws->copy, ws->ev[k], 0));
+    const size_t x0 = v0 < dv ? v0 : dv, x1 = v1 < dv ? v1 : dv;
+    if (x1 > x0)
+      TRY(cudaMemcpyAsync(x_prev + x0 * 3 * HW, static_cast<float *>(ws->xp.p) + x0 * 3 * HW,
+                          (x1 - x0) * 3 * HW * 4, cudaMemcpyDeviceToHost, ws->copy));
+    if (rgb)
+      TRY(cudaMemcpyAsync(rgb + v0 * 3 * HW, static_cast<float *>(ws->rgb.p) + v0 * 3 * HW,
+                          (v1 - v0) * 3 * HW * 4, cudaMemcpyDeviceToHost, ws->copy));
+    if (alpha)
+      TRY(cudaMemcpyAsync(alpha + v0 * HW, static_cast<float *>(ws->alpha.p) + v0 * HW,
+                          (v1 - v0) * HW * 4, cudaMemcpyDeviceToHost, ws->copy));
+  }
+  // the caller's stream completes after the last copy
+  TRY(cudaEventRecord(ws->ev[dmv3d_workspace::kChunks], ws->copy));
+  TRY(cudaStreamWaitEvent(st, ws->ev[dmv3d_workspace::kChunks], 0));
 #undef TRY
   return DMV3D_OK;
 }

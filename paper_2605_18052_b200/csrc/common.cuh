@@ -69,6 +69,8 @@ struct RenderParams {
   // interleaved ray tiles: tile_size > 0 keeps only the pixels of tiles
   // tau = (v ceil(H/T) + i/T) ceil(W/T) + j/T with tau mod tile_count == tile_rank
   int32_t tile_size, tile_rank, tile_count;
+  // host-pipelined step: G in the workspace is current (skip K0, only reset the counter)
+  int32_t reuse_g;
   // density grid mode of the tensor-core engine (row f3): G^3 points, x fastest
   int32_t grid_res;
   float *grid_sigma, *grid_rgb;

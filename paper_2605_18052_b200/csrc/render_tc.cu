@@ -692,8 +692,9 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // K0: G = F W0^T + b0 * bscale (fp16), zero the patch counter
-  cudaError_t e = launch_preproject(P, st);
+  // K0: G = F W0^T + b0 * bscale (fp16), zero the patch counter (a later ray-range launch
+  // of the same step reuses G and only resets the counter)
+  cudaError_t e = P.reuse_g ? cudaMemsetAsync(ws, 0, sizeof(unsigned int), st) : launch_preproject(P, st);
   if (e != cudaSuccess) return e;
   // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
