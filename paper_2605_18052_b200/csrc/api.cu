@@ -690,7 +690,7 @@ struct dmv3d_workspace {
   };
   Buf tp, intr, c2w, xt, z, xp, rgb, alpha, scratch, w[kMaxLayers], b[kMaxLayers];
   // copy-out pipeline: a stream for device->host copies and one event per view chunk
-  static constexpr int kChunks = 4;
+  static constexpr int kChunks = 2;
   cudaStream_t copy = nullptr;
   cudaEvent_t ev[kChunks + 1] = {};
   int dev = -1;
