@@ -232,8 +232,10 @@ dmv3d_status dmv3d_plucker_rays(const dmv3d_cameras *cams, const dmv3d_render_op
  *   L = sum grad_rgb * rgb + sum grad_alpha * alpha
  * w.r.t. the triplane and the MLP parameters, through the same rays, samples,
  * gather, MLP and quadrature as dmv3d_render_views -- the "differentiable volume
- * rendering" L_recon trains through.  No early termination
- * (opts.term_eps is ignored).  grad_rgb [V][3][H][W], grad_alpha [V][H][W] or
+ * rendering" L_recon trains through.  opts.term_eps > 0
+ * differentiates the early-terminated render (the forward engines' rule: a ray stops
+ * after the chunk where T < term_eps; later samples get no gradient); 0 = the full
+ * quadrature.  grad_rgb [V][3][H][W], grad_alpha [V][H][W] or
  * NULL; outputs are fp32 and ACCUMULATED (caller zeroes them): grad_triplane
  * [3][R][R][C], grad_weights / grad_biases = HOST arrays of L DEVICE pointers
  * shaped like W_l / b_l.  ReLU hidden layers only; atomics make the summation

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     // ---- pass 1: C and T_N (or the caller's forward render)
     float Tc = 1.0f, acc[3] = {0.f, 0.f, 0.f};
     const bool have_fwd = Gp.fwd_rgb != nullptr;
+    int kstop = P.N;  // the chunk after which the ray stopped (pass 1)
     if (have_fwd) {
       Tc = 1.0f - __ldg(Gp.fwd_alpha + (int64_t)v * HWp + pix);
 #pragma unroll
@@ -121,6 +122,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 #pragma unroll
       for (int c2 = 0; c2 < 3; ++c2) acc[c2] += w * c[c2];
       Tc *= expf(-__shfl_sync(0xffffffffu, S, 31));
+      if (P.term_eps > 0.0f && Tc < P.term_eps) {  // the forward's early termination
+        kstop = k0;
+        break;
+      }
     }
     float Ctot[3];
 #pragma unroll
@@ -334,6 +339,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
       Tc *= expf(-__shfl_sync(0xffffffffu, S, 31));
 #pragma unroll
       for (int q = 0; q < 3; ++q) Pc[q] += tot[q];
+      if (k0 == kstop || (have_fwd && P.term_eps > 0.0f && Tc < P.term_eps)) break;
     }
   }
 }

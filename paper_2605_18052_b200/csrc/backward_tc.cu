@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     ray.hit = false;
     ray.t_near = ray.t_far = 0.0f;
     if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
-    const bool alive = pix && ray.hit;
+    bool alive = pix && ray.hit;  // cleared when the ray terminates (T < term_eps)
     if (!ptx::bar_red_or(bar_id, 128, alive)) continue;
     const float delta = alive ? sample_delta(ray, P.N) : 0.0f;
     float gr[3] = {0.f, 0.f, 0.f}, gA = 0.0f;
@@ -472,6 +472,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
 #pragma unroll
       for (int e = 0; e < 3; ++e) acc[e] += w * c[e];
       T *= __expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
+      // early termination, the forward engine's rule: the ray stops after the chunk
+      if (alive && P.term_eps > 0.0f && T < P.term_eps) alive = false;
+      if (!ptx::bar_red_or(bar_id, 128, alive)) break;
     }
     float Ctot[3];
 #pragma unroll
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
     // ---------------- pass 2: forward again, then back through compositing and the MLP
     T = 1.0f;
+    alive = pix && ray.hit;
     float Pc[3] = {0.f, 0.f, 0.f};
     for (int k0 = 0; k0 < P.N; k0 += kChunk) {
       float o[4];
@@ -522,6 +526,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         Pc[e] += __shfl_sync(0xffffffffu, sc, kChunk - 1, kChunk);
       }
       T *= __expf(-__shfl_sync(0xffffffffu, S, kChunk - 1, kChunk));
+      const bool stop_after = alive && P.term_eps > 0.0f && T < P.term_eps;
       float d4[4] = {0.f, 0.f, 0.f, 0.f};
       if (sv) {
         const float cs = w * (1.0f + 2.0f * P.weps);
@@ -620,6 +625,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
         }
         ptx::tc_fence_before();
       }
+      if (stop_after) alive = false;
+      if (!ptx::bar_red_or(bar_id, 128, alive)) break;  // every ray of the patch stopped
       ptx::bar_sync(bar_id, 128);  // TMEM reads and table reads done before the next chunk
     }
   }

@@ -160,3 +160,36 @@ def test_backward_from_forward_outputs(engine, rel):
     oF, oW, ob = oracle.render_backward(tp, cams, m, N, g, gA, bg=bg)
     _check((dF.cpu().numpy(), [x.cpu().numpy() for x in dW], [x.cpu().numpy() for x in db],
             oF, oW, ob), rel=rel)
+
+
+@pytest.mark.parametrize("engine", ["tcgen05", "simt"])
+def test_backward_of_the_terminated_render(engine):
+    """opts.term_eps > 0: the gradient of the early-terminated render.  The first march
+    and the caller's terminated forward give the same gradient, and it stays within the
+    engine's bar of the full quadrature's (the dropped samples weigh T < term_eps)."""
+    C, L, H, W, N, eps = 32, 4, 10, 9, 40, 1e-3
+    tp = wl.round_to_bf16(wl.blob_triplane(12, C, seed=7, kappa=8.0))
+    m = wl.bf16_mlp(wl.blob_mlp(C, 64, L, seed=8))
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 2), wl.novel_cameras(H, W, 1, seed=9))
+    t, intr, c2w, mlp = dev_workload(wl.Workload("bwt", tp, cams, m, N, "bf16"))
+    rng = np.random.default_rng(4)
+    g = torch.from_numpy(rng.normal(size=(3, 3, H, W)).astype(np.float32)).cuda()
+    gA = torch.from_numpy(rng.normal(size=(3, H, W)).astype(np.float32)).cuda()
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    rgb, alpha = api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=N, engine=engine,
+                                        term_eps=eps, counters=cnt)
+    assert cnt[2].item() > 0  # some rays did terminate
+    a = api.dmv3d_render_backward(t, intr, c2w, H, W, mlp, g, gA, samples_per_ray=N,
+                                  engine=engine, term_eps=eps)
+    b = api.dmv3d_render_backward(t, intr, c2w, H, W, mlp, g, gA, samples_per_ray=N,
+                                  engine=engine, term_eps=eps, fwd=(rgb, alpha))
+    full = api.dmv3d_render_backward(t, intr, c2w, H, W, mlp, g, gA, samples_per_ray=N,
+                                     engine=engine)
+    torch.cuda.synchronize()
+    assert _rel_err(a[0].cpu().numpy(), b[0].cpu().numpy()) < 1e-3
+    for l in range(L):
+        assert _rel_err(a[1][l].cpu().numpy(), b[1][l].cpu().numpy()) < 1e-3
+    bar = REL if engine == "tcgen05" else 1e-2
+    assert _rel_err(a[0].cpu().numpy(), full[0].cpu().numpy()) < bar
+    for l in range(L):
+        assert _rel_err(a[1][l].cpu().numpy(), full[1][l].cpu().numpy()) < bar

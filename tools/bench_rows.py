@@ -181,6 +181,25 @@ def main():
                 "roofline": {"bound": "tensor", "achieved": fl2, "peak": bf, "unit": "TFLOP/s",
                              "frac": fl2 / bf, "kernel": "render_bwd_tc_kernel",
                              "algorithmic": f"{per_tc} FLOP per sample x {samples} hit samples"}})
+    # training with early ray termination (term_eps = 1e-4 in the forward and the backward)
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    rgb_t, alpha_t = api.dmv3d_render_views(tp, intr, c2w, 128, 128, mlp, samples_per_ray=128,
+                                            engine="tcgen05", term_eps=1e-4, counters=cnt)
+
+    def f1tc_term(timer):
+        api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
+                                  timer=timer, engine="tcgen05", term_eps=1e-4, fwd=(rgb_t, alpha_t))
+    kt_ms = timed(f1tc_term, args.reps, flush)
+    callt_ms = call_time(f1tc_term)
+    ev = int(cnt[1].item())  # samples the terminated forward evaluated (= the backward's)
+    fl3 = ev * per_tc / (kt_ms / 1e3) / 1e12
+    out.append({"row": "f1 renderer backward (tcgen05, term_eps 1e-4, given the forward)",
+                "metric": "rays/s", "value": rays / (callt_ms / 1e3), "call_ms": callt_ms,
+                "kernel_ms": kt_ms, "evaluated_samples": ev,
+                "config": "as above; forward and backward stop a ray once T < 1e-4",
+                "roofline": {"bound": "tensor", "achieved": fl3, "peak": bf, "unit": "TFLOP/s",
+                             "frac": fl3 / bf, "kernel": "render_bwd_tc_kernel",
+                             "algorithmic": f"{per_tc} FLOP per evaluated sample x {ev}"}})
     for line in out:
         print(json.dumps(line))
 
