@@ -100,7 +100,8 @@ def _check(res, rel=REL):
 
 
 @pytest.mark.parametrize("C,L,agg", [(80, 4, "mean"), (32, 4, "mean"), (16, 3, "sum"),
-                                     (8, 2, "mean"), (16, 4, "concat")])
+                                     (8, 2, "mean"), (16, 4, "concat"),
+                                     (16, 5, "mean"), (32, 7, "mean")])  # L >= 5: one group per SM
 def test_backward_tc_matches_oracle(C, L, agg):
     _check(_run(C, L, agg))
 
