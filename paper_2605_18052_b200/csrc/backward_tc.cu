@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
           if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
           else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
           else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; }
-          const int rr = loc / bw;
+          // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate reciprocal
+          // is never off by one
+          const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
           texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
         }
         sh->coltex[g][tid] = texel;
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     // this row's sparse A row of window [w0, w0 + kp): 12 bilinear weights (+ bias column)
     auto scatter_a = [&](int w0) {
       const int kp = min(kKW, ktot - w0);
+      const bool one_window = ktot <= kKW;
 #pragma unroll
       for (int kc = 0; kc < kKW / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
       if (!sv) return;
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if ((unsigned)cs[e] < (unsigned)kp)
+          if (one_window || (unsigned)cs[e] < (unsigned)kp)  // one window holds every column
             ptx::sts16(sArow + (uint32_t)(((cs[e] >> 3) << 7) | ((cs[e] & 7) << 1)),
                        ptx::f32_to_f16(w4[e]));
       }
