@@ -706,62 +706,63 @@ __global__ void __launch_bounds__(256)
 }
 
 // dW0[o][cofs + c] += sum_t dG_t[o] F_t[c];  db0[o] += bscale sum_t dG_t[o] (+ the bias
-// row).  A block reduces a slice of one plane's texels: thread (o = tid % 64, part =
-// tid / 64) owns columns c = part, part + 4, ... (< C + 1; column C = the bias).
+// row).  A block reduces a slice of one plane's texels; thread c (< C + 1; column C is the
+// bias, F := bscale) accumulates the 64 outputs of its column over the slice, reading the
+// staged dG rows as shared-memory broadcasts.
 constexpr int kWgTex = 32;
-constexpr int kWgMaxCols = 65;  // ceil((256 + 1) / 4)
 template <bool FP8>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(288)
     bwd_dw0_kernel(const float *__restrict__ dG, const void *__restrict__ Fv, float fscale, int C,
                    int R, int cat, int wstride, float bscale, int bias_row, float *__restrict__ dW0,
                    float *__restrict__ db0, int tex_per_block) {
-  __shared__ float sg[kWgTex][kHD];
-  __shared__ float sf[kWgTex][257];
-  const int tid = threadIdx.x, o = tid & 63, part = tid >> 6;
+  __shared__ float4 sg[kWgTex][kHD / 4];
+  const int c = threadIdx.x;
   const int64_t RR = (int64_t)R * R;
   const int64_t ntex = 3 * RR;
   const int64_t t0 = (int64_t)blockIdx.x * tex_per_block;
   const int64_t t1 = min(ntex, t0 + tex_per_block);
   const int plane = (int)(t0 / RR);  // tex_per_block divides R*R: one plane per block
-  float acc[kWgMaxCols];
+  float acc[kHD];
 #pragma unroll
-  for (int j = 0; j < kWgMaxCols; ++j) acc[j] = 0.0f;
+  for (int o = 0; o < kHD; ++o) acc[o] = 0.0f;
   for (int64_t tb = t0; tb < t1; tb += kWgTex) {
     const int nt = (int)min((int64_t)kWgTex, t1 - tb);
     __syncthreads();
-    for (int e = tid; e < nt * kHD; e += 256) sg[e / kHD][e % kHD] = dG[(tb + e / kHD) * kHD + e % kHD];
-    for (int e = tid; e < nt * (C + 1); e += 256) {
-      const int tt = e / (C + 1), c = e - tt * (C + 1);
-      float fv = bscale;
-      if (c < C) {
-        if constexpr (FP8) {
-          const __half_raw hr = __nv_cvt_fp8_to_halfraw(
-              static_cast<const __nv_fp8_storage_t *>(Fv)[(tb + tt) * C + c], __NV_E4M3);
-          fv = fscale * __half2float(__half(hr));
-        } else {
-          fv = __bfloat162float(static_cast<const __nv_bfloat16 *>(Fv)[(tb + tt) * C + c]);
-        }
-      }
-      sf[tt][c] = fv;
-    }
+    for (int e = threadIdx.x; e < nt * (kHD / 4); e += blockDim.x)
+      sg[e / (kHD / 4)][e % (kHD / 4)] = reinterpret_cast<const float4 *>(dG + (tb + e / (kHD / 4)) * kHD)[e % (kHD / 4)];
     __syncthreads();
-    for (int tt = 0; tt < nt; ++tt) {
-      const float gv = sg[tt][o];
+    if (c <= C) {
+      for (int tt = 0; tt < nt; ++tt) {
+        float fv = bscale;
+        if (c < C) {
+          if constexpr (FP8) {
+            const __half_raw hr = __nv_cvt_fp8_to_halfraw(
+                static_cast<const __nv_fp8_storage_t *>(Fv)[(tb + tt) * C + c], __NV_E4M3);
+            fv = fscale * __half2float(__half(hr));
+          } else {
+            fv = __bfloat162float(static_cast<const __nv_bfloat16 *>(Fv)[(tb + tt) * C + c]);
+          }
+        }
 #pragma unroll
-      for (int j = 0; j < kWgMaxCols; ++j) {
-        const int c = part + 4 * j;
-        if (c <= C) acc[j] += gv * sf[tt][c];
+        for (int o4 = 0; o4 < kHD / 4; ++o4) {
+          const float4 gv = sg[tt][o4];
+          acc[4 * o4] += gv.x * fv;
+          acc[4 * o4 + 1] += gv.y * fv;
+          acc[4 * o4 + 2] += gv.z * fv;
+          acc[4 * o4 + 3] += gv.w * fv;
+        }
       }
     }
   }
   const int cofs = cat ? plane * C : 0;
+  if (c < C) {
 #pragma unroll
-  for (int j = 0; j < kWgMaxCols; ++j) {
-    const int c = part + 4 * j;
-    if (c < C) atomicAdd(dW0 + (size_t)o * wstride + cofs + c, acc[j]);
-    else if (c == C && acc[j] != 0.0f) atomicAdd(db0 + o, acc[j]);
+    for (int o = 0; o < kHD; ++o) atomicAdd(dW0 + (size_t)o * wstride + cofs + c, acc[o]);
+  } else if (c == C && bscale != 0.0f) {
+#pragma unroll
+    for (int o = 0; o < kHD; ++o) atomicAdd(db0 + o, acc[o]);
   }
-  if (blockIdx.x == 0 && bias_row && tid < kHD) atomicAdd(db0 + tid, dG[ntex * kHD + tid]);
+  if (blockIdx.x == 0 && bias_row && threadIdx.x < kHD) atomicAdd(db0 + threadIdx.x, dG[ntex * kHD + threadIdx.x]);
 }
 
 template <int NG>
@@ -816,7 +817,8 @@ cudaError_t launch_render_backward_tc(const RenderParams &P0, const GradParams &
   int tpb = (int)((3 * RR + 2 * sms - 1) / (2 * sms));
   while (RR % tpb) ++tpb;
   const float bscale = P.smode != 0 ? 0.0f : (P.agg == 0 ? 1.0f : (1.0f / 3.0f));
-  (P.tp_fp8 ? bwd_dw0_kernel<true> : bwd_dw0_kernel<false>)<<<(int)((3 * RR) / tpb), 256, 0, st>>>(
+  const int nthr = ((C + 1) + 31) / 32 * 32;  // one thread per column of dW0 (+ the bias)
+  (P.tp_fp8 ? bwd_dw0_kernel<true> : bwd_dw0_kernel<false>)<<<(int)((3 * RR) / tpb), nthr, 0, st>>>(
       dG, P.tp, P.tp_scale, C, R, cat ? 1 : 0, wstride, bscale,
       P.smode != 0 ? 1 : 0, Gp.dW[0], Gp.db[0], tpb);
   return cudaGetLastError();
