@@ -60,6 +60,7 @@ constexpr int kTcHD = 64;       // hidden width of the tensor-core engine
 constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
+constexpr int kGridKZ = 4;      // density grid: 8x4x4 point blocks per patch column (chunks)
 constexpr uint32_t kWsHeader = kTcWsHeader;
 
 // shared-memory carve-up (bytes)
@@ -264,7 +265,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int v_lo = (int)(P.ray_begin / HW);
   const int v_hi = (int)((P.ray_end - 1) / HW);
   const int PH = (P.H + kPatch - 1) / kPatch, PW = (P.W + kPatch - 1) / kPatch;
-  const int GB[3] = {(P.grid_res + 7) / 8, (P.grid_res + 3) / 4, (P.grid_res + 3) / 4};
+  // density grid: a "patch" is a column of kGridKZ blocks of 8x4x4 points along z, walked
+  // as chunks so the next block's staging overlaps the current block's MLP
+  const int GB[3] = {(P.grid_res + 7) / 8, (P.grid_res + 3) / 4,
+                     (P.grid_res + 4 * kGridKZ - 1) / (4 * kGridKZ)};
   // interleaved ray tiles (§8e): the work queue enumerates this rank's tiles' patches
   const int TP = P.tile_size / kPatch;  // patches per tile side (0: no tiling)
   int64_t tile_first = 0, tile_n = 0;
@@ -352,20 +356,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
     Ray ray;
     ray.hit = false;
     ray.t_near = ray.t_far = 0.0f;
-    float gp[3] = {0.f, 0.f, 0.f};  // GRID: this row's grid point
+    int gx = 0, gy = 0, gz0 = 0;  // GRID: this row's point column (x, y) and first z
     if constexpr (GRID) {
       const int G = P.grid_res;
       const int bx = (int)(patch % GB[0]), by = (int)((patch / GB[0]) % GB[1]),
                 bz = (int)(patch / ((int64_t)GB[0] * GB[1]));
-      const int id3[3] = {bx * 8 + (tid & 7), by * 4 + ((tid >> 3) & 3), bz * 4 + (tid >> 5)};
-      pix = id3[0] < G && id3[1] < G && id3[2] < G;
-      r = ((int64_t)id3[2] * G + id3[1]) * G + id3[0];
-      const float gm1 = __int2float_rn(G - 1);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const float s = __fdiv_rn(__int2float_rn(id3[a]), gm1);
-        gp[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
-      }
+      gx = bx * 8 + (tid & 7);
+      gy = by * 4 + ((tid >> 3) & 3);
+      gz0 = bz * 4 * kGridKZ + (tid >> 5);
+      pix = gx < G && gy < G;
       ray.hit = pix;
     } else {
       int prow, pcol;
@@ -411,16 +410,21 @@ __global__ void __launch_bounds__(128 * NG, 1)
       par = chunk_ctr & 1;
       ++chunk_ctr;
       const int k = kk + q;
-      const bool sv = spec_alive && (GRID || k < P.N);  // GRID: one point per row
+      // GRID: one point per row, z advancing 4 per chunk
+      const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : k < P.N);
       ix[0] = ix[1] = ix[2] = 0;
       wl[0] = wl[1] = wl[2] = 0.f;
       wh[0] = wh[1] = wh[2] = 0.f;
       if (sv) {
         float p[3];
         if constexpr (GRID) {
-          p[0] = gp[0];
-          p[1] = gp[1];
-          p[2] = gp[2];
+          const int id3[3] = {gx, gy, gz0 + (kk / kChunk) * 4};
+          const float gm1 = __int2float_rn(P.grid_res - 1);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float s = __fdiv_rn(__int2float_rn(id3[a]), gm1);
+            p[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
+          }
         } else {
           const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
           sample_p(ray, sample_t(ray, delta, k, u), p);
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
     PH(0);
     for (int k0 = 0; have;) {
       const int k = k0 + q;
-      const bool sv = alive && (GRID || k < P.N);
+      const int gz = gz0 + (k0 / kChunk) * 4;  // GRID: this chunk's z
+      const bool sv = alive && (GRID ? gz < P.grid_res : k < P.N);
       const int *bb = sh->bbox[g][par];
       const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
@@ -513,7 +518,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
       // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
       const int k1 = k0 + kChunk;
-      const bool nxt = !GRID && k1 < P.N;
+      const bool nxt = GRID ? (k1 / kChunk < kGridKZ && gz0 - (tid >> 5) + (k1 / kChunk) * 4 < P.grid_res)
+                            : k1 < P.N;
       if (nxt) prefetch(k1, alive);
       PH(3);
 
@@ -563,14 +569,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
       if constexpr (GRID) {
         if (sv) {
           const int64_t n3 = (int64_t)P.grid_res * P.grid_res * P.grid_res;
-          P.grid_sigma[r] = sigma;
+          const int64_t rg = ((int64_t)gz * P.grid_res + gy) * P.grid_res + gx;
+          P.grid_sigma[rg] = sigma;
           if (P.grid_rgb) {
-            P.grid_rgb[r] = c0;
-            P.grid_rgb[n3 + r] = c1;
-            P.grid_rgb[2 * n3 + r] = c2;
+            P.grid_rgb[rg] = c0;
+            P.grid_rgb[n3 + rg] = c1;
+            P.grid_rgb[2 * n3 + rg] = c2;
           }
         }
-        have = false;
+        k0 = k1;
+        have = nxt;  // uniform over the group: no vote
         continue;
       }
       // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
@@ -702,7 +710,7 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   timer_begin(P.timer, st);
   if (grid_mode) {
     const int Gr = P.grid_res;
-    const int64_t nb = (int64_t)((Gr + 7) / 8) * ((Gr + 3) / 4) * ((Gr + 3) / 4);
+    const int64_t nb = (int64_t)((Gr + 7) / 8) * ((Gr + 3) / 4) * ((Gr + 4 * kGridKZ - 1) / (4 * kGridKZ));
     e = ng4 ? launch_k1<4, true>(P, sms, nb, st) : launch_k1<2, true>(P, sms, nb, st);
   } else {
     const int64_t HW = (int64_t)P.H * P.W;
