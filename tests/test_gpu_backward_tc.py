@@ -194,3 +194,52 @@ def test_backward_of_the_terminated_render(engine):
     assert _rel_err(a[0].cpu().numpy(), full[0].cpu().numpy()) < bar
     for l in range(L):
         assert _rel_err(a[1][l].cpu().numpy(), full[1][l].cpu().numpy()) < bar
+
+
+def test_backward_tc_directional_derivatives_at_cfg2_size():
+    """Full BASELINE configs[1] size (4 views 128^2, N = 128, 3x64x64x80, MLP 80-64-64-64-4),
+    in the launch configuration the rows bench times: the tensor-core gradient, contracted
+    with random directions of the triplane and of every weight matrix, equals the central
+    difference of L = <g, rgb> + <gA, alpha> through the fp32 SIMT forward (a property of
+    any size; the oracle's full backward at this size takes minutes)."""
+    w = wl.make_workload("cfg2_bf16")
+    V, H, W, N = w.cameras.num_views, w.cameras.height, w.cameras.width, w.samples_per_ray
+    t, intr, c2w, mlp = dev_workload(w)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    g = torch.randn((V, 3, H, W), device="cuda", generator=gen)
+    gA = torch.randn((V, H, W), device="cuda", generator=gen)
+    dF, dW, db = api.dmv3d_render_backward(t, intr, c2w, H, W, mlp, g, gA, samples_per_ray=N,
+                                           engine="tcgen05")
+    tp32 = t.float()
+    w32 = [x.float() for x in mlp.weights]
+
+    def loss(tp_, ws_):
+        m = api.DeviceMLP(ws_, mlp.biases, "f32")
+        rgb, alpha = api.dmv3d_render_views(tp_, intr, c2w, H, W, m, samples_per_ray=N,
+                                            engine="simt")
+        return float((g.double() * rgb.double()).sum() + (gA.double() * alpha.double()).sum())
+
+    cases = [("F", dF)] + [(f"W{l}", dW[l]) for l in range(len(dW))]
+    for name, grad in cases:
+        d = torch.randn(grad.shape, device="cuda", generator=gen)
+        if name in ("W1", "W2"):
+            # the benchmark MLP's hidden unit 0 passes the density through (row 0 =
+            # [1, 0, ...]): outside the blob its pre-activation is exactly 0, i.e. ON the
+            # ReLU kink, where a central difference averages the one-sided slopes while
+            # the gradient takes relu'(0) = 0.  Directions that leave row 0 alone keep
+            # every perturbed pre-activation generic (tools/fd_probe.py shows the gap).
+            d[0, :] = 0.0
+        base = tp32 if name == "F" else w32[int(name[1:])]
+        eps = 1e-3 * float(base.abs().max())
+        d = d / d.abs().max()
+
+        def shifted(sgn):
+            if name == "F":
+                return loss(tp32 + sgn * eps * d, w32)
+            ws_ = list(w32)
+            ws_[int(name[1:])] = w32[int(name[1:])] + sgn * eps * d
+            return loss(tp32, ws_)
+        fd = (shifted(1.0) - shifted(-1.0)) / (2 * eps)
+        an = float((grad.double() * d.double()).sum())
+        print(f"{name}: analytic {an:.6g} central difference {fd:.6g}")
+        assert abs(an - fd) <= 3e-2 * abs(fd) + 1e-3, (name, an, fd)
