@@ -377,6 +377,10 @@ def main():
               "compulsory_bytes_per_step": comp_b,
               "compulsory_gbs": comp_b / ks / 1e9,
               "compulsory_frac_of_hbm": comp_b / ks / 1e9 / peaks["hbm_gbs"],
+              # (i) of §8d: against the on-chip L1/shared-memory bandwidth, 128 B/clk/SM
+              "l1_smem_peak_gbs": 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9,
+              "requested_frac_of_l1_smem": eval_samples * req_b / ks / 1e9
+              / (148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9),
               "dram_gbs_ncu": ncu / ks / 1e9 if ncu else None,
               "l2_hit_pct_ncu": l2hit}
 
