@@ -15,7 +15,7 @@
 // group owns a 4x4-pixel patch (16 rays) and walks it twice in chunks of 8 samples
 // (tile = 128 rows = 16 rays x 8 samples):
 //   pass 1: forward (blend MMA + L-1 layer MMAs) and compositing -> C = sum w c + T_N bg
-//           and T_N per ray;
+//           and T_N per ray (skipped when the caller passes its forward's rgb / alpha);
 //   pass 2: forward again, keeping every layer's fp16 input h_l in shared memory,
 //           then per sample dC/dtau_k = T_{k+1} c_k - R_k, R_k = C - sum_{j<=k} w_j c_j
 //           (8-lane scans), dC/dc_k = w_k, dA/dtau_k = T_N -> the head delta d_o
@@ -26,9 +26,11 @@
 //             dz_{l-1} = dh_l (.) [h_l > 0]          (written over h_l's tile)
 //             dG_window = A_blend^T dz0              (the blend's own sparse A tile,
 //                                                     MN-major; rows = staged texels)
-//           dG rows go to the workspace with 16-B vector reductions; the dW/db
-//           accumulators live in TMEM for the whole launch (shared by the groups) and
-//           are added to the caller's buffers once per CTA.
+//           dG rows go to the workspace with 16-B vector reductions; each group's dW/db
+//           accumulators live in TMEM for the whole launch and are added to the
+//           caller's buffers once per CTA.  The dh and dW K-steps of a trip are issued
+//           interleaved (independent accumulation chains overlap in the tensor pipe;
+//           one chain's dependent steps do not).
 // K2/K3 map dG back to dF, dW0 and db0 (fp32 CUDA cores, 2 x 63 MFLOP at R = 64).
 //
 // Shared-memory operand layouts are SWIZZLE_NONE core matrices (8 rows x 16 B):
@@ -36,8 +38,9 @@
 // M/N (tools/mma_layout_check.cu verifies this on the B200).  A tile written by its
 // row threads as [row][col] with 16-B chunks of 8 columns serves both as a K-major
 // operand (rows = M) and as an MN-major one (rows = K).
-// No early termination (opts.term_eps is ignored): the gradient is exact up to the
-// fp16 operand rounding (tolerances).
+// opts.term_eps > 0 differentiates the early-terminated render (the forward's rule, per
+// 8-sample chunk); otherwise the full quadrature.  Exact up to the fp16 operand rounding
+// (tolerances).
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 
