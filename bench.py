@@ -163,6 +163,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "rays_per_step_sampled": rays_per_step},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
                              "sample": f"{rays_per_step} random rays of {args.config} per step (of "
                                        f"{w.num_rays}), full 128-sample march, fp64, no early "
                                        "termination"},
@@ -392,6 +393,7 @@ def main():
         cpu = {"value": r_rate, "unit": "rays/s", "cores": threads, "kind": "oracle",
                "sample": f"{n_rays} random rays of {args.config} (of {rays}) in {secs:.1f} s; full "
                          f"128-sample march, fp64, no early termination"}
+        cpu["cpu_model"] = _cpu_model()
         # the oracle is also timed on one core
         r1, n1, s1 = oracle_rate(w, args.cpu_budget / 3, 1, seed=8)
         cpu["single_core"] = {"value": r1, "unit": "rays/s", "cores": 1,
@@ -428,6 +430,17 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def _tc_available(api, tp, intr, c2w, H, W, mlp):
