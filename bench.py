@@ -184,13 +184,15 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--mode", default="assets", choices=["assets", "views", "views-p2p", "tiles"],
+    ap.add_argument("--mode", default="assets",
+                    choices=["assets", "views", "views-p2p", "tiles", "tiles-p2p"],
                     help="assets: one asset per rank, no data-path collective (weak scaling, "
                          "default); views: one asset's views split across ranks with an NCCL "
                          "triplane broadcast + all-gather per step (strong scaling); views-p2p: "
                          "the same split, outputs assembled by the render kernel's NVLink peer "
                          "stores into symmetric memory; tiles: one asset's 16x16 ray tiles dealt "
-                         "round robin to the ranks, outputs assembled by one all-reduce")
+                         "round robin to the ranks, outputs assembled by one all-reduce; tiles-p2p: "
+                         "the same, assembled by the render kernel's NVLink peer stores")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -213,7 +215,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs (one asset per rank, seeds 100 + rank), resident in HBM
-    views_mode = args.mode in ("views", "views-p2p", "tiles")
+    views_mode = args.mode in ("views", "views-p2p", "tiles", "tiles-p2p")
     wname, metric, workload = CONFIGS[args.config]
     w = wl.make_workload(wname, asset=rank if (world > 1 and not views_mode) else None)
     V, H, W = w.cameras.num_views, w.cameras.height, w.cameras.width
@@ -238,11 +240,12 @@ def main():
 
     def step(i, x_in, x_out, cnt=None, timer=None):
         t, tp_ = pairs[i % len(pairs)]
-        if args.mode == "tiles" and world > 1:
+        if args.mode in ("tiles", "tiles-p2p") and world > 1:
             from paper_2605_18052_b200 import dist as pdist
             xp, _, _ = pdist.denoise_step_tile_sharded(
                 tp, intr, c2w, H, W, mlp, ab, t, tp_, x_in, DV, samples_per_ray=w.samples_per_ray,
-                term_eps=TERM_EPS, engine=args.engine, counters=cnt, timer=timer)
+                term_eps=TERM_EPS, engine=args.engine, counters=cnt, timer=timer,
+                p2p=args.mode == "tiles-p2p")
             x_out.copy_(xp)
             return
         if views_mode and world > 1:
@@ -410,7 +413,9 @@ def main():
                            "l2": "flushed between timed steps (256 MiB write); triplane re-read "
                                  "from HBM each step",
                            "parallelism": (f"16x16 ray tiles interleaved x{world} (NCCL broadcast "
-                                           "+ all-reduce)" if args.mode == "tiles" else
+                                           + ("+ NVLink peer stores)" if args.mode == "tiles-p2p"
+                                              else "+ all-reduce)")
+                                           if args.mode.startswith("tiles") else
                                            f"view-sharded x{world} (NCCL broadcast + "
                                            + ("NVLink peer stores)" if args.mode == "views-p2p"
                                               else "all-gather)")

@@ -173,12 +173,29 @@ def tile_owner(v: int, i: int, j: int, height: int, width: int, tile: int, world
 def denoise_step_tile_sharded(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
                               x_t, ddim_views: int, group=None, src: int = 0,
                               broadcast_triplane: bool = True, render_fn=None, tile: int = 16,
-                              **opts):
+                              p2p: bool = False, **opts):
     """One denoising step of one asset, T x T ray tiles dealt round robin to the ranks.
-    Returns the full (x_prev, rgb, alpha) on every rank."""
+    Returns the full (x_prev, rgb, alpha) on every rank.  `p2p`: outputs in symmetric
+    memory, every rank's render epilogue stores its pixels into all peers' buffers at the
+    same offsets (no all-reduce; one device-side barrier)."""
     render_fn = render_fn or default_render_fn
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if p2p and world > 1:
+        V = int(c2w.shape[0])
+        if broadcast_triplane:
+            dist.broadcast(triplane, src=src, group=group)
+        (xp, rgb, alpha), (hx, hr, ha) = _symm_outputs(
+            [(max(ddim_views, 1), 3, height, width), (V, 3, height, width), (V, height, width)],
+            triplane.device, group)
+        peers = {"rgb": peer_pointers(hr.buffer_ptrs, rank, 0),
+                 "alpha": peer_pointers(ha.buffer_ptrs, rank, 0),
+                 "x_prev": peer_pointers(hx.buffer_ptrs, rank, 0) if ddim_views else []}
+        render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
+                  x_t if ddim_views else None, xp[:ddim_views] if ddim_views else None, rgb, alpha,
+                  tiles=(tile, rank, world), peers=peers, **opts)
+        ha.barrier()
+        return xp[:ddim_views], rgb, alpha
     V = int(c2w.shape[0])
     dev = triplane.device
     if broadcast_triplane and world > 1:

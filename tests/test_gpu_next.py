@@ -205,3 +205,31 @@ def test_interleaved_tiles_union_is_the_full_step(engine, dtype, T, P):
         m2 = mine[:2].unsqueeze(1).expand_as(xp)
         u_xp[m2] = sx[m2]
     assert torch.equal(u_a, alpha) and torch.equal(u_rgb, rgb) and torch.equal(u_xp, xp)
+
+
+@pytest.mark.parametrize("engine,dtype", [("tcgen05", "bf16"), ("simt", "f32")])
+def test_tiles_with_peer_stores(engine, dtype):
+    """tiles-p2p: a rank's render epilogue stores exactly its tiles' pixels into every
+    peer buffer at the same offsets (peers emulated by local buffers on one GPU)."""
+    from paper_2605_18052_b200 import dist as pdist
+    tp = wl.blob_triplane(12, 32, seed=2)
+    m = wl.blob_mlp(32, 64, 4, seed=3)
+    if dtype == "bf16":
+        tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
+    H, W, T, P = 21, 18, 8, 3
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 2), wl.novel_cameras(H, W, 1, seed=4))
+    t, intr, c2w, mlp = dev_workload(wl.Workload("tp2p", tp, cams, m, 16, dtype))
+    rgb, alpha = api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=16, engine=engine)
+    owner = torch.tensor([[[pdist.tile_owner(v, i, j, H, W, T, P) for j in range(W)]
+                           for i in range(H)] for v in range(3)], device="cuda")
+    for r in range(P):
+        pr = [torch.full_like(rgb, -7.0) for _ in range(2)]
+        pa = [torch.full_like(alpha, -7.0) for _ in range(2)]
+        api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=16, engine=engine,
+                               tiles=(T, r, P), peers={"rgb": [x.data_ptr() for x in pr],
+                                                       "alpha": [x.data_ptr() for x in pa]})
+        mine = owner == r
+        for k in range(2):
+            assert torch.equal(pa[k][mine], alpha[mine]) and (pa[k][~mine] == -7.0).all()
+            m3 = mine.unsqueeze(1).expand_as(rgb)
+            assert torch.equal(pr[k][m3], rgb[m3]) and (pr[k][~m3] == -7.0).all()
