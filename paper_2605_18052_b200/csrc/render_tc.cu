@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(256)
                       float bscale, float fscale, __half *__restrict__ G, unsigned int *counter,
                       __half *__restrict__ gbias) {
   extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
-  for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {
-    const int o = e / C, c = e - o * C;
+  for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {  // o fastest: conflict-free stores
+    const int c = e / kTcHD, o = e - c * kTcHD;
     reinterpret_cast<float *>(swt)[c * kTcHD + o] = __bfloat162float(W0[(size_t)o * wstride + c]);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && counter) *counter = 0u;
@@ -122,8 +122,15 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bias0 = __ldg(b0 + 2 * lane) * bscale, bias1 = __ldg(b0 + 2 * lane + 1) * bscale;
-  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntex;
-       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  const int64_t t_first = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t t_step = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // bf16: lane q holds 16-B chunk q of the texel row (C <= 256: <= 32 chunks), loaded in
+  // one round trip and one texel ahead; the dot products read the chunks by shuffle
+  const int nq = FP8 ? 0 : C / 8;
+  uint4 cur = make_uint4(0u, 0u, 0u, 0u);
+  if (!FP8 && t_first < ntex && lane < nq)
+    cur = __ldg(reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(Fv) + t_first * C) + lane);
+  for (int64_t t = t_first; t < ntex; t += t_step) {
     float a0 = bias0, a1 = bias1;
     if constexpr (FP8) {
       const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint8_t *>(Fv) + t * C);
@@ -145,20 +152,28 @@ __global__ void __launch_bounds__(256)
       a0 += fscale * s0;
       a1 += fscale * s1;
     } else {
-      const __nv_bfloat16 *F = static_cast<const __nv_bfloat16 *>(Fv);
-      const uint4 *src = reinterpret_cast<const uint4 *>(F + t * C);
-      for (int q = 0; q < C / 8; ++q) {
-        const uint4 u = __ldg(src + q);  // same address across the warp: one broadcast request
-        const uint32_t uv[4] = {u.x, u.y, u.z, u.w};
+      const int64_t tn = t + t_step;
+      uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
+      if (tn < ntex && lane < nq)
+        nxt = __ldg(reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(Fv) + tn * C) + lane);
+      float b0s = 0.0f, b1s = 0.0f;  // second pair of partial sums: two chains per output
+      for (int q = 0; q < nq; ++q) {
+        const uint32_t uv[4] = {__shfl_sync(0xffffffffu, cur.x, q), __shfl_sync(0xffffffffu, cur.y, q),
+                                __shfl_sync(0xffffffffu, cur.z, q), __shfl_sync(0xffffffffu, cur.w, q)};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 w0 = swt[(q * 8 + 2 * e) * (kTcHD / 2) + lane];
           const float2 w1 = swt[(q * 8 + 2 * e + 1) * (kTcHD / 2) + lane];
           const float f0 = bf16lo(uv[e]), f1 = bf16hi(uv[e]);
-          a0 += w0.x * f0 + w1.x * f1;
-          a1 += w0.y * f0 + w1.y * f1;
+          a0 += w0.x * f0;
+          a1 += w0.y * f0;
+          b0s += w1.x * f1;
+          b1s += w1.y * f1;
         }
       }
+      a0 += b0s;
+      a1 += b1s;
+      cur = nxt;
     }
     const uint32_t pk = (uint32_t)ptx::f32_to_f16(a0) | ((uint32_t)ptx::f32_to_f16(a1) << 16);
     reinterpret_cast<uint32_t *>(G + t * kTcHD)[lane] = pk;
