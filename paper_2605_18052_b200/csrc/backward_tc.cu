@@ -812,7 +812,7 @@ cudaError_t launch_render_backward_tc(const RenderParams &P0, const GradParams &
   e = cudaFuncSetAttribute(bwd_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   if (e != cudaSuccess) return e;
   int g2 = (int)((ntex * 32 + 255) / 256);
-  if (g2 > sms * 8) g2 = sms * 8;
+  if (g2 > sms * 2) g2 = sms * 2;  // W0 block staged once per block
   bwd_df_kernel<<<g2, 256, s2, st>>>(dG, W0, wstride, C, R, cat ? 1 : 0, Gp.dF);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // texels per K3 block: a divisor of R*R near R*R*3/(2 sms)
