@@ -279,9 +279,11 @@ def main():
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             flush.zero_()
+            torch.cuda.nvtx.range_push(f"denoise step {k}")  # NVTX range per loop step
             starts[k].record(stream)
             step(args.warmup + k, xa, xb, timer=kernel_timer)
             ends[k].record(stream)
+            torch.cuda.nvtx.range_pop()
             xa, xb = xb, xa
         barrier()
     step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
