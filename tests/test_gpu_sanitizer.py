@@ -1,0 +1,27 @@
+"""compute-sanitizer over every CUDA entry point on small inputs
+(tools/sanitize.py) on the GPU box: no memory errors, no shared-memory races."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool,clean", [("memcheck", "ERROR SUMMARY: 0 errors"),
+                                        ("racecheck", "0 hazards displayed (0 errors, 0 warnings)")])
+def test_compute_sanitizer_clean(tool, clean):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([exe, "--tool", tool, sys.executable, "tools/sanitize.py"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert "sanitize workload done" in out, out[-2000:]
+    assert clean in out, out[-2000:]
