@@ -256,3 +256,13 @@ def test_fp8_triplane_needs_tc_engine():
         api.dmv3d_render_views(t8, intr, c2w, cams.height, cams.width, mlp, samples_per_ray=8,
                                engine="simt")
     assert e.value.status == 2  # UNSUPPORTED
+
+
+def test_fp8_triplane_density_grid_tc():
+    vals, m, cams, t8, intr, c2w, mlp = _fp8_setup(0.75)
+    G = 19
+    sigma, rgb = api.dmv3d_density_grid(t8, mlp, G, engine="tcgen05", fp8_scale=0.75)
+    osig, orgb = oracle.density_grid(vals, m, G)
+    s = sigma.cpu().numpy()
+    assert np.max(np.abs(s - osig) / np.maximum(1.0, osig)) < RGB_TOL
+    assert np.max(np.abs(rgb.cpu().numpy() - orgb)) < RGB_TOL
