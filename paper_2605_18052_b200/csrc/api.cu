@@ -746,6 +746,8 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
   CHECK_ARG(mlp->weights && mlp->biases, "mlp: weights / biases array is NULL");
   CHECK_ARG(cams->num_views >= 1 && cams->height >= 1 && cams->width >= 1, "cameras: V, H, W must be >= 1");
   CHECK_ARG(ddim->ddim_views >= 1 && ddim->ddim_views <= cams->num_views, "ddim: need 1 <= ddim_views <= V");
+  if (opts->tile_size)  // the full outputs are copied back: a tile shard would return stale pixels
+    return fail(DMV3D_ERR_UNSUPPORTED, "host step: interleaved tiles are a device-buffer option");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t V = cams->num_views, HW = (size_t)cams->height * cams->width;
   const size_t tp_bytes = (size_t)3 * triplane->res * triplane->res * triplane->channels *
