@@ -232,7 +232,7 @@ def main():
     rgb = torch.empty((V, 3, H, W), device=dev)
     alpha = torch.empty((V, H, W), device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev)
-    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
     rays = V * H * W
     stream = torch.cuda.current_stream(dev)
 
@@ -427,6 +427,9 @@ def main():
                 "hit_fraction": hit_frac,
                 "terminated_fraction_of_hit": cnt[2] / max(cnt[0], 1),
                 "evaluated_fraction_of_nominal": eval_samples / (rays * w.samples_per_ray),
+                # tensor-core tiles: evaluated samples / MMA rows issued, mean staged K
+                "mma_row_occupancy": (eval_samples / cnt[4]) if cnt[4] > 0 else None,
+                "mean_blend_k": (cnt[5] / (cnt[4] / 128)) if cnt[4] > 0 else None,
                 "roofline": roof, "gather_roofline": gather, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},

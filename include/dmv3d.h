@@ -121,9 +121,13 @@ typedef struct {
   int64_t ray_begin, ray_end; /* shard [begin, end) of global ray ids; -1,-1 = all.
                               Only pixels of the shard are written.                    */
   dmv3d_engine engine;
-  unsigned long long *counters; /* optional DEVICE [4] accumulators (NULL = off):
+  unsigned long long *counters; /* optional DEVICE [8] accumulators (NULL = off):
                               [0] rays hit, [1] samples evaluated,
-                              [2] rays terminated early, [3] rays processed           */
+                              [2] rays terminated early, [3] rays processed,
+                              TCGEN05 only: [4] tensor-core tile rows issued (128 per
+                              blend window: evaluated / issued = MMA row occupancy),
+                              [5] staged texel columns (K) summed over blend windows,
+                              [6..7] reserved (0)                                      */
   void *workspace;         /* DEVICE scratch of >= dmv3d_workspace_bytes() bytes, 256-B
                               aligned; required by the TCGEN05 engine (holds the
                               per-step projected triplane), ignored by SIMT.  One

@@ -28,8 +28,11 @@
 //         update (row a6).
 //    The NG groups interleave on the SM: while one group waits on its MMA
 //    chain the others stage, scatter and run epilogues.
+#include <cuda.h>  // CUtensorMap types only (the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
+
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -62,6 +65,13 @@ constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
 constexpr int kGridKZ = 4;      // density grid: 8x4x4 point blocks per patch column (chunks)
 constexpr uint32_t kWsHeader = kTcWsHeader;
+// window column layout: plane p's e_a x e_b texels start at a multiple of kPlaneAlign
+// columns (8 x 128 B = one SWIZZLE_128B atom: a TMA box lands atom-aligned)
+#ifndef DMV3D_PLANE_ALIGN
+#define DMV3D_PLANE_ALIGN 8
+#endif
+constexpr int kPlaneAlign = DMV3D_PLANE_ALIGN;
+__host__ __device__ constexpr int plane_pad(int n) { return (n + kPlaneAlign - 1) & ~(kPlaneAlign - 1); }
 
 // shared-memory carve-up (bytes)
 constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;    // 32 KiB, K-major, SBO 2048
@@ -90,6 +100,9 @@ struct TcShared {
   int bbox[NG][2][8];  // per chunk parity: xmin,ymin,zmin,-,xmax,ymax,zmax,-
   int coltex[NG][kTcKMax];  // staged column -> texel index of G (-1: zero fill)
   float head_bias[4];
+  unsigned n_tiles[NG], n_kcols[NG];  // blend windows issued, staged K columns (counters[4..5])
+  unsigned n_tma[NG];                 // windows staged by TMA boxes (counters[6])
+  uint64_t tbar[NG];                  // TMA completion of the staged window
 };
 
 template <int NG>
@@ -211,7 +224,7 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 // 128-row tile through the same staged-texel blend + MLP MMAs.
 template <int NG, bool GRID>
 __global__ void __launch_bounds__(128 * NG, 1)
-    render_tc_kernel(const __grid_constant__ RenderParams P) {
+    render_tc_kernel(const __grid_constant__ RenderParams P, const __grid_constant__ TmaMaps M) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -229,7 +242,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
   // ---- prologue: barriers, TMEM, weights (fp16, K-major, bias column)
   if (tid_cta == 0) {
-    for (int i = 0; i < NG; ++i) ptx::mbar_init(&sh->mbar[i], 1);
+    for (int i = 0; i < NG; ++i) {
+      ptx::mbar_init(&sh->mbar[i], 1);
+      ptx::mbar_init(&sh->tbar[i], 1);
+      sh->n_tiles[i] = sh->n_kcols[i] = sh->n_tma[i] = 0u;
+    }
     for (int i = 0; i < NG; ++i)
       for (int p = 0; p < 2; ++p)
         for (int e = 0; e < 8; ++e) sh->bbox[i][p][e] = (e < 4) ? 0x7fffffff : -1;
@@ -256,6 +273,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
     }
   }
   if (tid_cta < 4) sh->head_bias[tid_cta] = __ldg(P.b[L - 1] + tid_cta);
+  // B tiles start zeroed: TMA-staged windows leave the padding columns [ktex, kpad) as
+  // the previous chunk left them (finite G values times zero A weights)
+  for (uint32_t e = tid_cta; e < NG * kBTileBytes / 16; e += 128 * NG)
+    reinterpret_cast<uint4 *>(tileB0)[e] = make_uint4(0u, 0u, 0u, 0u);
+  const bool use_tma = M.valid != 0 && P.smode == 0;
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -301,8 +323,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // that reads the bias row G[3 R R]
   const int hb = P.smode != 0 ? 1 : 0;
 
-  uint32_t mphase = 0;
-  unsigned long long n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;
+  uint32_t mphase = 0, tphase = 0;
+  unsigned n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;  // per thread: fits 32 bits
   PH_DECL
   int chunk_ctr = 0;
 
@@ -315,7 +337,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   auto fill_table = [&](const int *bb, int w0, bool direct) {
     const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
     const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
-    const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
+    const int base1 = plane_pad(ext0 * ext1), base2 = base1 + plane_pad(ext0 * ext2);
     const int ktex = base2 + ext1 * ext2;
     const int ktot = ktex + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
@@ -326,13 +348,14 @@ __global__ void __launch_bounds__(128 * NG, 1)
         texel = 3 * R * R;
       } else if (kg < ktex) {
         int loc, bw, ta0, tb0, pl;
-        if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
-        else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
-        else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; }
+        int np;  // texels of the plane (columns up to its padded base are zero)
+        if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; np = ext1 * ext2; }
+        else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; np = ext0 * ext2; }
+        else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; np = ext0 * ext1; }
         // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate
         // reciprocal is never off by one
         const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
-        texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
+        texel = loc < np ? (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw) : -1;
       }
       sh->coltex[g][tid] = texel;
       if (direct) {  // this thread stages texel row tid itself: no table round trip
@@ -349,7 +372,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // SWIZZLE_128B (16-B chunk index XOR row index within each 1 KiB atom)
   auto stage = [&](const int *bb, int w0) {
     const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-    const int ktot = e0 * e1 + e0 * e2 + e1 * e2 + hb;
+    const int ktot = plane_pad(e0 * e1) + plane_pad(e0 * e2) + e1 * e2 + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     for (int e = tid; e < kpad * 8; e += 128) {
       const int kl = e >> 3, ch = e & 7;
@@ -419,6 +442,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
     int ix[3] = {0, 0, 0};
     float wl[3] = {0.f, 0.f, 0.f}, wh[3] = {0.f, 0.f, 0.f};  // weights of texels ix, ix + 1
     int par = 0;
+    bool tma_staged = false;  // window 0 of the prepared chunk is staged by TMA boxes ...
+    bool tma_used = false;    // ... and its completion has been consumed
     // geometry + window + staging of window 0 for the chunk starting at kk (the
     // chunk's bbox slot must still hold its reset state when this runs)
     auto prefetch = [&](int kk, bool spec_alive) {
@@ -464,7 +489,28 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ptx::bar_sync(bar_id, 128);
       // reset the other parity's slot for the next chunk (all its readers passed a barrier)
       if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
-      fill_table(sh->bbox[g][par], 0, true);
+      const int *bb = sh->bbox[g][par];
+      const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
+      // TMA: one box per plane (plane p's e_a x e_b texel rows land at its window base);
+      // larger windows take the per-texel cp.async path
+      tma_staged = use_tma && max(e0, max(e1, e2)) <= kTmaMaxExt &&
+                   plane_pad(e0 * e1) + plane_pad(e0 * e2) + e1 * e2 <= kTcKMax;  // one window
+      tma_used = false;
+      if (tma_staged) {
+        if (tid == 0) {
+          const int b1 = plane_pad(e0 * e1), b2 = b1 + plane_pad(e0 * e2);
+          constexpr int kE = kTmaMaxExt - 1;
+          ptx::mbar_arrive_expect_tx(&sh->tbar[g], (uint32_t)(e0 * e1 + e0 * e2 + e1 * e2) * (kTcHD * 2));
+          ptx::tma_load_4d(sB, M.map[(e0 - 2) * kE + (e1 - 2)], &sh->tbar[g], 0, bb[0], bb[1], 0);
+          ptx::tma_load_4d(sB + (uint32_t)(b1 * kTcHD * 2), M.map[(e0 - 2) * kE + (e2 - 2)], &sh->tbar[g],
+                           0, bb[0], bb[2], 1);
+          ptx::tma_load_4d(sB + (uint32_t)(b2 * kTcHD * 2), M.map[(e1 - 2) * kE + (e2 - 2)], &sh->tbar[g],
+                           0, bb[1], bb[2], 2);
+          sh->n_tma[g] += 1u;
+        }
+      } else {
+        fill_table(bb, 0, true);
+      }
     };
 
     bool have = ptx::bar_red_or(bar_id, 128, alive);
@@ -478,7 +524,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
       // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); row-major bbox rows
-      const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
+      const int base1 = plane_pad(ext0 * ext1), base2 = base1 + plane_pad(ext0 * ext2);
       const int ktex = base2 + ext1 * ext2;
       const int ktot = ktex + hb;
       const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
@@ -518,15 +564,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
         ptx::bar_sync(bar_id, 128);
         if (tid == 0) {
           ptx::tc_fence_after();
+          if (w0 == 0 && tma_staged) ptx::mbar_wait_bounded(&sh->tbar[g], tphase);
           for (int ks = 0; ks < kpad / 16; ++ks) {
             const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
             const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
             ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
+          sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
+          sh->n_kcols[g] += (unsigned)kpad;
         }
         ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
+        if (w0 == 0 && tma_staged) {
+          tphase ^= 1u;
+          tma_used = true;
+        }
       }
       ptx::tc_fence_after();
       PH(2);
@@ -620,6 +673,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
       PH(6);
     }
     ptx::cp_async_wait_all();  // a prefetch for a chunk nobody needs may still be landing
+    if (tma_staged && !tma_used) {  // ... or its TMA boxes: drain them (barrier phase, B tile)
+      if (tid == 0) ptx::mbar_wait_bounded(&sh->tbar[g], tphase);
+      tphase ^= 1u;
+    }
     // ---- ray epilogue: reduce the 8 lanes, write rgb/alpha (+ DDIM x_{t-1})
 #pragma unroll
     for (int s = kChunk / 2; s > 0; s >>= 1) {
@@ -643,10 +700,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
       n_rays += __shfl_xor_sync(0xffffffffu, n_rays, s);
     }
     if ((tid & 31) == 0) {
-      atomicAdd(P.counters + 0, n_hit);
-      atomicAdd(P.counters + 1, n_samples);
-      atomicAdd(P.counters + 2, n_term);
-      atomicAdd(P.counters + 3, n_rays);
+      atomicAdd(P.counters + 0, (unsigned long long)n_hit);
+      atomicAdd(P.counters + 1, (unsigned long long)n_samples);
+      atomicAdd(P.counters + 2, (unsigned long long)n_term);
+      atomicAdd(P.counters + 3, (unsigned long long)n_rays);
+    }
+    if (tid == 0) {  // MMA rows issued (128 per blend window) and staged K columns
+      atomicAdd(P.counters + 4, 128ull * sh->n_tiles[g]);
+      atomicAdd(P.counters + 5, (unsigned long long)sh->n_kcols[g]);
+      atomicAdd(P.counters + 6, (unsigned long long)sh->n_tma[g]);
     }
   }
   ptx::tc_fence_before();
@@ -658,6 +720,63 @@ __global__ void __launch_bounds__(128 * NG, 1)
 }
 
 // ------------------------------------------------------------------ launch
+// ------------------------------------------------------------------ TMA tensor maps
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); the
+// maps of a workspace are encoded once and cached by (G address, R).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool encode_maps(TmaMaps &m, const void *G, int R) {
+  static EncodeTiledFn fn = nullptr;
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  if (!fn || R < kTmaMaxExt) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)kTcHD, (cuuint64_t)R, (cuuint64_t)R, 3};
+  const cuuint64_t strides[3] = {(cuuint64_t)kTcHD * 2, (cuuint64_t)kTcHD * 2 * R,
+                                 (cuuint64_t)kTcHD * 2 * R * R};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  for (int ea = 2; ea <= kTmaMaxExt; ++ea)
+    for (int eb = 2; eb <= kTmaMaxExt; ++eb) {
+      const cuuint32_t box[4] = {(cuuint32_t)kTcHD, (cuuint32_t)ea, (cuuint32_t)eb, 1};
+      CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(m.map[(ea - 2) * (kTmaMaxExt - 1) + (eb - 2)]);
+      if (fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void *>(G), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+  return true;
+}
+
+static TmaMaps tma_maps(const void *G, int R) {  // by value: the cache entry may be reused
+  struct Entry {
+    const void *G;
+    int R;
+    TmaMaps m;
+  };
+  static std::mutex mu;
+  static Entry cache[8];
+  static int n = 0, next = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < n; ++i)
+    if (cache[i].G == G && cache[i].R == R) return cache[i].m;
+  Entry &e = cache[next];
+  next = (next + 1) % 8;
+  n = n < 8 ? n + 1 : 8;
+  e.G = G;
+  e.R = R;
+  e.m.valid = (getenv("DMV3D_NO_TMA") == nullptr && encode_maps(e.m, G, R)) ? 1 : 0;
+  return e.m;
+}
+
 template <int NG, bool GRID>
 static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
   const size_t s1 = tc_smem_bytes<NG>(P.L);
@@ -666,7 +785,8 @@ static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cud
   if (e != cudaSuccess) return e;
   int grid = sms;
   if ((int64_t)grid * NG > npatch) grid = (int)((npatch + NG - 1) / NG);
-  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P);
+  const TmaMaps maps = tma_maps(static_cast<const uint8_t *>(P.tp) + kWsHeader, P.R);
+  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P, maps);
   return cudaGetLastError();
 }
 

@@ -176,7 +176,7 @@ def test_backward_of_the_terminated_render(engine):
     rng = np.random.default_rng(4)
     g = torch.from_numpy(rng.normal(size=(3, 3, H, W)).astype(np.float32)).cuda()
     gA = torch.from_numpy(rng.normal(size=(3, H, W)).astype(np.float32)).cuda()
-    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
     rgb, alpha = api.dmv3d_render_views(t, intr, c2w, H, W, mlp, samples_per_ray=N, engine=engine,
                                         term_eps=eps, counters=cnt)
     assert cnt[2].item() > 0  # some rays did terminate

@@ -193,8 +193,8 @@ def test_termination_bound_and_counters():
     w = _mid_workload()
     tp, intr, c2w, mlp = dev_workload(w)
     H, W = w.cameras.height, w.cameras.width
-    cnt0 = torch.zeros(4, dtype=torch.int64, device="cuda")
-    cnt1 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cnt0 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    cnt1 = torch.zeros(8, dtype=torch.int64, device="cuda")
     full, afull = api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, samples_per_ray=w.samples_per_ray,
                                          term_eps=0.0, counters=cnt0)
     eps = 1e-3

@@ -36,7 +36,7 @@ def _wl(C=80, L=4, R=64, H=48, W=40, N=128, views_in=2, views_novel=1, seed=1, b
 def _tc_render(w, term_eps=1e-4, ids=None, bg=(1.0, 1.0, 1.0), agg="mean", **kw):
     tp, intr, c2w, mlp = dev_workload(w)
     H, W = w.cameras.height, w.cameras.width
-    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
     rgb, alpha = api.dmv3d_render_views(tp, intr, c2w, H, W, mlp, samples_per_ray=w.samples_per_ray,
                                         term_eps=term_eps, engine="tcgen05", bg=bg, agg=agg,
                                         counters=cnt, **kw)

@@ -182,7 +182,7 @@ def main():
                              "frac": fl2 / bf, "kernel": "render_bwd_tc_kernel",
                              "algorithmic": f"{per_tc} FLOP per sample x {samples} hit samples"}})
     # training with early ray termination (term_eps = 1e-4 in the forward and the backward)
-    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
     rgb_t, alpha_t = api.dmv3d_render_views(tp, intr, c2w, 128, 128, mlp, samples_per_ray=128,
                                             engine="tcgen05", term_eps=1e-4, counters=cnt)
 

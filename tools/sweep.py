@@ -61,7 +61,7 @@ def main():
             xb = torch.empty_like(xa)
             rgb = torch.empty((V, 3, S, S), device=dev)
             alpha = torch.empty((V, S, S), device=dev)
-            cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+            cnt = torch.zeros(8, dtype=torch.int64, device=dev)
             timer = api.Timer()
 
             def step(i, x_in, x_out, counters=None, tm=None):
