@@ -28,11 +28,8 @@
 //         update (row a6).
 //    The NG groups interleave on the SM: while one group waits on its MMA
 //    chain the others stage, scatter and run epilogues.
-#include <cuda.h>  // CUtensorMap types only (the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
-
-#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -64,14 +61,8 @@ constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
 constexpr int kGridKZ = 4;      // density grid: 8x4x4 point blocks per patch column (chunks)
+constexpr uint32_t kHeadCol = kTcHD + 40;  // head output: 16 TMEM columns after the fp16 A operand
 constexpr uint32_t kWsHeader = kTcWsHeader;
-// window column layout: plane p's e_a x e_b texels start at a multiple of kPlaneAlign
-// columns (8 x 128 B = one SWIZZLE_128B atom: a TMA box lands atom-aligned)
-#ifndef DMV3D_PLANE_ALIGN
-#define DMV3D_PLANE_ALIGN 8
-#endif
-constexpr int kPlaneAlign = DMV3D_PLANE_ALIGN;
-__host__ __device__ constexpr int plane_pad(int n) { return (n + kPlaneAlign - 1) & ~(kPlaneAlign - 1); }
 
 // shared-memory carve-up (bytes)
 constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;    // 32 KiB, K-major, SBO 2048
@@ -101,8 +92,6 @@ struct TcShared {
   int coltex[NG][kTcKMax];  // staged column -> texel index of G (-1: zero fill)
   float head_bias[4];
   unsigned n_tiles[NG], n_kcols[NG];  // blend windows issued, staged K columns (counters[4..5])
-  unsigned n_tma[NG];                 // windows staged by TMA boxes (counters[6])
-  uint64_t tbar[NG];                  // TMA completion of the staged window
 };
 
 template <int NG>
@@ -224,7 +213,7 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 // 128-row tile through the same staged-texel blend + MLP MMAs.
 template <int NG, bool GRID>
 __global__ void __launch_bounds__(128 * NG, 1)
-    render_tc_kernel(const __grid_constant__ RenderParams P, const __grid_constant__ TmaMaps M) {
+    render_tc_kernel(const __grid_constant__ RenderParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -244,8 +233,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   if (tid_cta == 0) {
     for (int i = 0; i < NG; ++i) {
       ptx::mbar_init(&sh->mbar[i], 1);
-      ptx::mbar_init(&sh->tbar[i], 1);
-      sh->n_tiles[i] = sh->n_kcols[i] = sh->n_tma[i] = 0u;
+      sh->n_tiles[i] = sh->n_kcols[i] = 0u;
     }
     for (int i = 0; i < NG; ++i)
       for (int p = 0; p < 2; ++p)
@@ -273,11 +261,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
     }
   }
   if (tid_cta < 4) sh->head_bias[tid_cta] = __ldg(P.b[L - 1] + tid_cta);
-  // B tiles start zeroed: TMA-staged windows leave the padding columns [ktex, kpad) as
-  // the previous chunk left them (finite G values times zero A weights)
-  for (uint32_t e = tid_cta; e < NG * kBTileBytes / 16; e += 128 * NG)
-    reinterpret_cast<uint4 *>(tileB0)[e] = make_uint4(0u, 0u, 0u, 0u);
-  const bool use_tma = M.valid != 0 && P.smode == 0;
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -323,7 +306,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // that reads the bias row G[3 R R]
   const int hb = P.smode != 0 ? 1 : 0;
 
-  uint32_t mphase = 0, tphase = 0;
+  uint32_t mphase = 0;
   unsigned n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;  // per thread: fits 32 bits
   PH_DECL
   int chunk_ctr = 0;
@@ -337,9 +320,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
   auto fill_table = [&](const int *bb, int w0, bool direct) {
     const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
     const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
-    const int base1 = plane_pad(ext0 * ext1), base2 = base1 + plane_pad(ext0 * ext2);
+    const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
     const int ktex = base2 + ext1 * ext2;
-    const int ktot = ktex + hb;
+    const int ktot = bb[4] < 0 ? 0 : ktex + hb;  // bb[4] < 0: no valid row (empty window)
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     if (tid < kpad) {
       const int kg = w0 + tid;
@@ -348,14 +331,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
         texel = 3 * R * R;
       } else if (kg < ktex) {
         int loc, bw, ta0, tb0, pl;
-        int np;  // texels of the plane (columns up to its padded base are zero)
-        if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; np = ext1 * ext2; }
-        else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; np = ext0 * ext2; }
-        else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; np = ext0 * ext1; }
+        if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
+        else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
+        else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; }
         // row = floor(loc / bw): loc < 2^13 and bw < 2^8, so an approximate
         // reciprocal is never off by one
         const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
-        texel = loc < np ? (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw) : -1;
+        texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
       }
       sh->coltex[g][tid] = texel;
       if (direct) {  // this thread stages texel row tid itself: no table round trip
@@ -372,7 +354,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // SWIZZLE_128B (16-B chunk index XOR row index within each 1 KiB atom)
   auto stage = [&](const int *bb, int w0) {
     const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-    const int ktot = plane_pad(e0 * e1) + plane_pad(e0 * e2) + e1 * e2 + hb;
+    const int ktot = bb[4] < 0 ? 0 : e0 * e1 + e0 * e2 + e1 * e2 + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     for (int e = tid; e < kpad * 8; e += 128) {
       const int kl = e >> 3, ch = e & 7;
@@ -389,7 +371,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
     if (patch >= npatch) break;
     PH(7);
     int v = 0, i = 0, j = 0;
-    int64_t r = 0;
     bool pix;
     Ray ray;
     ray.hit = false;
@@ -421,7 +402,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       i = prow * kPatch + (slot >> 2);
       j = pcol * kPatch + (slot & 3);
-      r = (int64_t)v * HW + (int64_t)i * P.W + j;
+      const int64_t r = (int64_t)v * HW + (int64_t)i * P.W + j;
       pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
       if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
       if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
@@ -434,24 +415,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
       n_hit += alive ? 1 : 0;
     }
 
-    // Chunk pipeline: the geometry, texel window and cp.async staging of chunk
-    // c+1 are issued while chunk c's MLP runs on the tensor cores (the staged B
-    // tile is free once c's blend MMA has completed).  Chunk c+1 is prepared for
-    // the rays alive before c's compositing; rays that terminate in c get zero A
-    // rows in c+1.
-    int ix[3] = {0, 0, 0};
-    float wl[3] = {0.f, 0.f, 0.f}, wh[3] = {0.f, 0.f, 0.f};  // weights of texels ix, ix + 1
+    // Chunk pipeline (per group, chunk c = samples [k0, k0 + 8) of the 16 rays):
+    //   top:     wait for {blend(c), head(c-1)}; composite c-1 (head read from TMEM
+    //            columns kHeadCol..); rare extra blend windows of c
+    //   layers:  epilogue -> hidden layer MMAs of c (one round trip each); in the
+    //            first layer's MMA shadow the geometry, texel window, B staging and
+    //            sparse-A scatter of chunk c+1 are prepared (for the rays alive after
+    //            c-1's compositing: rays that terminate in c get one wasted chunk)
+    //   bottom:  ONE commit issues head(c) and blend(c+1): three MMA round trips per
+    //            chunk instead of four.
+    // The head writes its own 16 TMEM columns (kHeadCol), so blend(c+1) can overwrite
+    // the accumulator while head(c)'s result waits to be composited.
     int par = 0;
-    bool tma_staged = false;  // window 0 of the prepared chunk is staged by TMA boxes ...
-    bool tma_used = false;    // ... and its completion has been consumed
-    // geometry + window + staging of window 0 for the chunk starting at kk (the
-    // chunk's bbox slot must still hold its reset state when this runs)
-    auto prefetch = [&](int kk, bool spec_alive) {
-      par = chunk_ctr & 1;
-      ++chunk_ctr;
-      const int k = kk + q;
-      // GRID: one point per row, z advancing 4 per chunk
-      const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : k < P.N);
+    bool sv_n = false;  // this row's sample is valid in the prepared chunk
+    // a1-a3 for this row's sample of the chunk starting at kk: texel cell per axis
+    // (weights of texels ix, ix + 1)
+    auto geometry = [&](int kk, bool sv, int (&ix)[3], float (&wl)[3], float (&wh)[3]) {
       ix[0] = ix[1] = ix[2] = 0;
       wl[0] = wl[1] = wl[2] = 0.f;
       wh[0] = wh[1] = wh[2] = 0.f;
@@ -466,13 +445,25 @@ __global__ void __launch_bounds__(128 * NG, 1)
             p[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
           }
         } else {
-          const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
+          const int k = kk + q;
+          const float u = P.jitter ? jitter_u(P.seed, (uint64_t)(((int64_t)v * P.H + i) * P.W + j) * P.N + k)
+                                   : 0.5f;
           sample_p(ray, sample_t(ray, delta, k, u), p);
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
           texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
       }
+    };
+    // geometry + window + staging of window 0 for the chunk starting at kk (the
+    // chunk's bbox slot must still hold its reset state when this runs)
+    auto prefetch = [&](int kk, bool spec_alive, int (&ix)[3], float (&wl)[3], float (&wh)[3]) {
+      par = chunk_ctr & 1;
+      ++chunk_ctr;
+      // GRID: one point per row, z advancing 4 per chunk
+      const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : kk + q < P.N);
+      sv_n = sv;
+      geometry(kk, sv, ix, wl, wh);
       int mn[3], mx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -489,140 +480,63 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ptx::bar_sync(bar_id, 128);
       // reset the other parity's slot for the next chunk (all its readers passed a barrier)
       if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
-      const int *bb = sh->bbox[g][par];
-      const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-      // TMA: one box per plane (plane p's e_a x e_b texel rows land at its window base);
-      // larger windows take the per-texel cp.async path
-      tma_staged = use_tma && max(e0, max(e1, e2)) <= kTmaMaxExt &&
-                   plane_pad(e0 * e1) + plane_pad(e0 * e2) + e1 * e2 <= kTcKMax;  // one window
-      tma_used = false;
-      if (tma_staged) {
-        if (tid == 0) {
-          const int b1 = plane_pad(e0 * e1), b2 = b1 + plane_pad(e0 * e2);
-          constexpr int kE = kTmaMaxExt - 1;
-          ptx::mbar_arrive_expect_tx(&sh->tbar[g], (uint32_t)(e0 * e1 + e0 * e2 + e1 * e2) * (kTcHD * 2));
-          ptx::tma_load_4d(sB, M.map[(e0 - 2) * kE + (e1 - 2)], &sh->tbar[g], 0, bb[0], bb[1], 0);
-          ptx::tma_load_4d(sB + (uint32_t)(b1 * kTcHD * 2), M.map[(e0 - 2) * kE + (e2 - 2)], &sh->tbar[g],
-                           0, bb[0], bb[2], 1);
-          ptx::tma_load_4d(sB + (uint32_t)(b2 * kTcHD * 2), M.map[(e1 - 2) * kE + (e2 - 2)], &sh->tbar[g],
-                           0, bb[1], bb[2], 2);
-          sh->n_tma[g] += 1u;
-        }
-      } else {
-        fill_table(bb, 0, true);
-      }
+      fill_table(sh->bbox[g][par], 0, true);
     };
-
-    bool have = ptx::bar_red_or(bar_id, 128, alive);
-    if (have) prefetch(0, alive);
-    PH(0);
-    for (int k0 = 0; have;) {
-      const int k = k0 + q;
-      const int gz = gz0 + (k0 / kChunk) * 4;  // GRID: this chunk's z
-      const bool sv = alive && (GRID ? gz < P.grid_res : k < P.N);
+    // sparse-A rows of window [w0, w0 + kTcKMax) of the prepared chunk; returns kpad
+    auto scatter = [&](int w0, const int (&ix)[3], const float (&wl)[3], const float (&wh)[3]) -> int {
       const int *bb = sh->bbox[g][par];
       const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
       // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); row-major bbox rows
-      const int base1 = plane_pad(ext0 * ext1), base2 = base1 + plane_pad(ext0 * ext2);
+      const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
       const int ktex = base2 + ext1 * ext2;
-      const int ktot = ktex + hb;
-      const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
-      const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
-      const int bws[3] = {ext0, ext0, ext1};
-      const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
-      const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
-
-      // ---- blend on the tensor cores: window 0 was staged by prefetch; rare extra
-      //      windows (> kTcKMax texels) are staged synchronously
-      for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
-        const int kp = min(kTcKMax, ktot - w0);
-        const int kpad = (kp + 15) & ~15;
-        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
-        if (sv) {
+      const int ktot = bb[4] < 0 ? 0 : ktex + hb;  // empty window: no valid row
+      const int kp = min(kTcKMax, ktot - w0);
+      const int kpad = (kp + 15) & ~15;
+      for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
+      if (sv_n) {
+        const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
+        const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
+        const int bws[3] = {ext0, ext0, ext1};
+        const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
+        const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
 #pragma unroll
-          for (int pl = 0; pl < 3; ++pl) {
-            const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
-            const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
-            const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
-            const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
+        for (int pl = 0; pl < 3; ++pl) {
+          const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
+          const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
+          const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
+          const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
-          }
-          if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
-            ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);  // fp16 1.0: + b0
+          for (int e = 0; e < 4; ++e)
+            if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
         }
-        if (w0 > 0) {  // synchronous staging of an extra window
-          fill_table(bb, w0, false);
-          ptx::bar_sync(bar_id, 128);
-          stage(bb, w0);
-        }
-        PH(1);
-        ptx::cp_async_wait_all();
-        ptx::fence_proxy_async_smem();
-        ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          if (w0 == 0 && tma_staged) ptx::mbar_wait_bounded(&sh->tbar[g], tphase);
-          for (int ks = 0; ks < kpad / 16; ++ks) {
-            const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
-            const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-            ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit(&sh->mbar[g]);
-          sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
-          sh->n_kcols[g] += (unsigned)kpad;
-        }
-        ptx::mbar_wait(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        if (w0 == 0 && tma_staged) {
-          tphase ^= 1u;
-          tma_used = true;
-        }
+        if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
+          ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);  // fp16 1.0: + b0
       }
-      ptx::tc_fence_after();
-      PH(2);
-
-      // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
-      const int k1 = k0 + kChunk;
-      const bool nxt = GRID ? (k1 / kChunk < kGridKZ && gz0 - (tid >> 5) + (k1 / kChunk) * 4 < P.grid_res)
-                            : k1 < P.N;
-      if (nxt) prefetch(k1, alive);
-      PH(3);
-
-      // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
-      //      (A operand from TMEM), weights in shared memory
-      for (int l = 1; l < L; ++l) {
-        act_epilogue(tmem_row, tmem_row + kTcHD);
-        PH(4);
-        ptx::tc_fence_before();
-        ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
-          const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
-          // the head skips its bias K block (4 FADDs at readout instead of an MMA)
-          const int nks = (l == L - 1) ? kTcHD / 16 : (int)kWK / 16;
-#pragma unroll
-          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            if (ks < nks) {
-              const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-              ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
-            }
-          }
-          ptx::mma_commit(&sh->mbar[g]);
-        }
-        ptx::mbar_wait(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        ptx::tc_fence_after();
-        PH(5);
+      return kpad;
+    };
+    auto window_total = [&]() {
+      const int *bb = sh->bbox[g][par];
+      const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
+      return bb[4] < 0 ? 0 : e0 * e1 + e0 * e2 + e1 * e2 + hb;
+    };
+    // blend MMAs of one window (issuing thread only)
+    auto issue_blend = [&](int kpad, bool acc) {
+      for (int ks = 0; ks < kpad / 16; ++ks) {
+        const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
+        const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
+        ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (acc || ks > 0) ? 1u : 0u);
       }
-      // ---- head: sigma, rgb (a4)
+      sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
+      sh->n_kcols[g] += (unsigned)kpad;
+    };
+    // head readout + compositing (a4 head, a5) of the chunk starting at kc
+    auto head_composite = [&](int kc, bool svc) {
       uint32_t o4[4];
-      ptx::tmem_ld4(tmem_row, o4);
+      ptx::tmem_ld4(tmem_row + kHeadCol, o4);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
+      const bool sv = alive && svc;
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
         const float *bh = sh->head_bias;  // shared memory: broadcast reads
@@ -636,6 +550,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       if constexpr (GRID) {
         if (sv) {
+          const int gz = gz0 + (kc / kChunk) * 4;
           const int64_t n3 = (int64_t)P.grid_res * P.grid_res * P.grid_res;
           const int64_t rg = ((int64_t)gz * P.grid_res + gy) * P.grid_res + gx;
           P.grid_sigma[rg] = sigma;
@@ -645,11 +560,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
             P.grid_rgb[2 * n3 + rg] = c2;
           }
         }
-        k0 = k1;
-        have = nxt;  // uniform over the group: no vote
-        continue;
+        return;
       }
-      // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
+      // a5: composite the ray's 8 samples (8-lane segmented scan)
       const float tau = sv ? sigma * delta : 0.0f;
       float S = tau;
 #pragma unroll
@@ -665,18 +578,142 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const float Stot = __shfl_sync(0xffffffffu, S, kChunk - 1, kChunk);
       T = T * __expf(-Stot);
       if (alive && P.term_eps > 0.0f && T < P.term_eps) {
-        if (nxt && q == 0) n_term++;
+        if (kc + kChunk < P.N && q == 0) n_term++;
         alive = false;
       }
-      k0 = k1;
-      have = nxt && ptx::bar_red_or(bar_id, 128, alive);
+    };
+    // is there a chunk after the one starting at kk (uniform over the group)
+    auto has_next = [&](int kk) {
+      const int k1 = kk + kChunk;
+      return GRID ? (k1 / kChunk < kGridKZ && gz0 - (tid >> 5) + (k1 / kChunk) * 4 < P.grid_res)
+                  : k1 < P.N;
+    };
+
+    bool have = ptx::bar_red_or(bar_id, 128, alive);
+    if (have) {
+      int ix[3];
+      float wl[3], wh[3];
+      prefetch(0, alive, ix, wl, wh);
+      const int kpad = scatter(0, ix, wl, wh);
+      ptx::cp_async_wait_all();
+      ptx::fence_proxy_async_smem();
+      ptx::bar_sync(bar_id, 128);
+      if (tid == 0) {
+        ptx::tc_fence_after();
+        issue_blend(kpad, false);
+        ptx::mma_commit(&sh->mbar[g]);
+      }
+    }
+    PH(0);
+    bool sv_prev = false;  // chunk k0 - 8's rows (its head is in flight when k0 > 0)
+    for (int k0 = 0; have;) {
+      const bool sv_c = sv_n;  // validity of chunk k0's rows (as prepared)
+      ptx::mbar_wait(&sh->mbar[g], mphase);
+      mphase ^= 1u;
+      ptx::tc_fence_after();
+      PH(2);
+      if (k0 > 0) head_composite(k0 - kChunk, sv_prev);
       PH(6);
+      // ---- rare extra blend windows (> kTcKMax texels), staged synchronously
+      const int ktot = window_total();
+      for (int w0 = kTcKMax; w0 < ktot; w0 += kTcKMax) {
+        int ix[3];
+        float wl[3], wh[3];
+        geometry(k0, sv_c, ix, wl, wh);  // recomputed: not kept live across the layers
+        const int kpad = scatter(w0, ix, wl, wh);
+        fill_table(sh->bbox[g][par], w0, false);
+        ptx::bar_sync(bar_id, 128);
+        stage(sh->bbox[g][par], w0);
+        ptx::cp_async_wait_all();
+        ptx::fence_proxy_async_smem();
+        ptx::bar_sync(bar_id, 128);
+        if (tid == 0) {
+          ptx::tc_fence_after();
+          issue_blend(kpad, true);
+          ptx::mma_commit(&sh->mbar[g]);
+        }
+        ptx::mbar_wait(&sh->mbar[g], mphase);
+        mphase ^= 1u;
+        ptx::tc_fence_after();
+      }
+      const bool nxt = has_next(k0);
+      bool prepared = false;
+      auto prepare_next = [&]() {  // chunk k0 + 8: geometry, window, staging, A rows
+        if (nxt) {
+          int ix[3];
+          float wl[3], wh[3];
+          prefetch(k0 + kChunk, alive, ix, wl, wh);
+          scatter(0, ix, wl, wh);
+        }
+        prepared = true;
+        PH(3);
+      };
+#ifndef DMV3D_PREP_AT
+#define DMV3D_PREP_AT 0  // 0: in layer 1's MMA shadow; 1: before, 2: after the first epilogue
+#endif
+      if (DMV3D_PREP_AT == 1) prepare_next();
+      // ---- hidden layers 1..L-2 on the tensor cores: fp16 activations live in TMEM
+      //      (A operand from TMEM), weights in shared memory
+      bool any = true;
+      for (int l = 1; l < L - 1; ++l) {
+        act_epilogue(tmem_row, tmem_row + kTcHD);
+        PH(4);
+        if (DMV3D_PREP_AT == 2 && l == 1) prepare_next();
+        ptx::tc_fence_before();
+        if (l == 1) {
+          any = ptx::bar_red_or(bar_id, 128, alive);  // every ray of the patch done?
+          if (!any) break;
+        } else {
+          ptx::bar_sync(bar_id, 128);
+        }
+        if (tid == 0) {
+          ptx::tc_fence_after();
+          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
+#pragma unroll
+          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
+            const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
+            ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, idesc_hidden, ks > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&sh->mbar[g]);
+        }
+        if (DMV3D_PREP_AT == 0 && l == 1) prepare_next();
+        ptx::mbar_wait(&sh->mbar[g], mphase);
+        mphase ^= 1u;
+        ptx::tc_fence_after();
+        PH(5);
+      }
+      if (!any) break;
+      if (!prepared) prepare_next();  // L = 2: no hidden layer to hide it behind
+      // ---- head(c) and blend(c+1) in one commit
+      act_epilogue(tmem_row, tmem_row + kTcHD);
+      PH(4);
+      ptx::cp_async_wait_all();
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      const bool go = ptx::bar_red_or(bar_id, 128, nxt && alive);
+      if (tid == 0) {
+        ptx::tc_fence_after();
+        const uint32_t wbase = sW + (uint32_t)((L - 2) * kWHidden);
+        // the head skips its bias K block (4 FADDs at readout instead of an MMA)
+#pragma unroll
+        for (int ks = 0; ks < kTcHD / 16; ++ks) {
+          const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
+          ptx::mma_f16_ts(tmem + kHeadCol, tmem + kTcHD + ks * 8, bd, idesc_head, ks > 0 ? 1u : 0u);
+        }
+        if (go) issue_blend(min(kTcKMax, (window_total() + 15) & ~15), false);
+        ptx::mma_commit(&sh->mbar[g]);
+      }
+      sv_prev = sv_c;
+      k0 += kChunk;
+      if (!go) {  // last chunk of the patch: composite it now
+        ptx::mbar_wait(&sh->mbar[g], mphase);
+        mphase ^= 1u;
+        ptx::tc_fence_after();
+        head_composite(k0 - kChunk, sv_prev);
+        break;
+      }
     }
     ptx::cp_async_wait_all();  // a prefetch for a chunk nobody needs may still be landing
-    if (tma_staged && !tma_used) {  // ... or its TMA boxes: drain them (barrier phase, B tile)
-      if (tid == 0) ptx::mbar_wait_bounded(&sh->tbar[g], tphase);
-      tphase ^= 1u;
-    }
     // ---- ray epilogue: reduce the 8 lanes, write rgb/alpha (+ DDIM x_{t-1})
 #pragma unroll
     for (int s = kChunk / 2; s > 0; s >>= 1) {
@@ -708,7 +745,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
     if (tid == 0) {  // MMA rows issued (128 per blend window) and staged K columns
       atomicAdd(P.counters + 4, 128ull * sh->n_tiles[g]);
       atomicAdd(P.counters + 5, (unsigned long long)sh->n_kcols[g]);
-      atomicAdd(P.counters + 6, (unsigned long long)sh->n_tma[g]);
     }
   }
   ptx::tc_fence_before();
@@ -720,63 +756,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
 }
 
 // ------------------------------------------------------------------ launch
-// ------------------------------------------------------------------ TMA tensor maps
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); the
-// maps of a workspace are encoded once and cached by (G address, R).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static bool encode_maps(TmaMaps &m, const void *G, int R) {
-  static EncodeTiledFn fn = nullptr;
-  static bool looked = false;
-  if (!looked) {
-    looked = true;
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  if (!fn || R < kTmaMaxExt) return false;
-  const cuuint64_t dims[4] = {(cuuint64_t)kTcHD, (cuuint64_t)R, (cuuint64_t)R, 3};
-  const cuuint64_t strides[3] = {(cuuint64_t)kTcHD * 2, (cuuint64_t)kTcHD * 2 * R,
-                                 (cuuint64_t)kTcHD * 2 * R * R};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  for (int ea = 2; ea <= kTmaMaxExt; ++ea)
-    for (int eb = 2; eb <= kTmaMaxExt; ++eb) {
-      const cuuint32_t box[4] = {(cuuint32_t)kTcHD, (cuuint32_t)ea, (cuuint32_t)eb, 1};
-      CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(m.map[(ea - 2) * (kTmaMaxExt - 1) + (eb - 2)]);
-      if (fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void *>(G), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    }
-  return true;
-}
-
-static TmaMaps tma_maps(const void *G, int R) {  // by value: the cache entry may be reused
-  struct Entry {
-    const void *G;
-    int R;
-    TmaMaps m;
-  };
-  static std::mutex mu;
-  static Entry cache[8];
-  static int n = 0, next = 0;
-  std::lock_guard<std::mutex> lk(mu);
-  for (int i = 0; i < n; ++i)
-    if (cache[i].G == G && cache[i].R == R) return cache[i].m;
-  Entry &e = cache[next];
-  next = (next + 1) % 8;
-  n = n < 8 ? n + 1 : 8;
-  e.G = G;
-  e.R = R;
-  e.m.valid = (getenv("DMV3D_NO_TMA") == nullptr && encode_maps(e.m, G, R)) ? 1 : 0;
-  return e.m;
-}
-
 template <int NG, bool GRID>
 static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
   const size_t s1 = tc_smem_bytes<NG>(P.L);
@@ -785,8 +764,7 @@ static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cud
   if (e != cudaSuccess) return e;
   int grid = sms;
   if ((int64_t)grid * NG > npatch) grid = (int)((npatch + NG - 1) / NG);
-  const TmaMaps maps = tma_maps(static_cast<const uint8_t *>(P.tp) + kWsHeader, P.R);
-  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P, maps);
+  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P);
   return cudaGetLastError();
 }
 
