@@ -41,15 +41,6 @@ cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, 
 // render_tc.cu (tcgen05 / TMEM engine).  Workspace: [256-B header: patch counter]
 // [G: (3 R R + 1) x HD fp16] (+ for the backward, 256-B aligned: [dG: (3 R R + 1) x HD fp32])
 constexpr uint32_t kTcWsHeader = 256;
-// TMA staging of the texel window (one box per plane): tensor maps of G [3][R][R][HD]
-// fp16 (SWIZZLE_128B, one 128-B texel row per box row) for every box shape
-// (ea, eb) in [2, kTmaMaxExt]^2, index (ea - 2) * (kTmaMaxExt - 1) + (eb - 2)
-constexpr int kTmaMaxExt = 8;
-constexpr int kTmaMaps = (kTmaMaxExt - 1) * (kTmaMaxExt - 1);
-struct alignas(64) TmaMaps {
-  uint8_t map[kTmaMaps][128];  // CUtensorMap (opaque, 64-B aligned)
-  int32_t valid;               // 0: the driver entry point was unavailable (cp.async only)
-};
 bool tc_supported(int C, int HD, int L);  // C = triplane channels per plane
 size_t tc_workspace_bytes(int R, int HD);
 cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st);

@@ -61,7 +61,6 @@ constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
 constexpr int kGridKZ = 4;      // density grid: 8x4x4 point blocks per patch column (chunks)
-constexpr uint32_t kHeadCol = kTcHD + 40;  // head output: 16 TMEM columns after the fp16 A operand
 constexpr uint32_t kWsHeader = kTcWsHeader;
 
 // shared-memory carve-up (bytes)
@@ -322,7 +321,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
     const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
     const int ktex = base2 + ext1 * ext2;
-    const int ktot = bb[4] < 0 ? 0 : ktex + hb;  // bb[4] < 0: no valid row (empty window)
+    const int ktot = ktex + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     if (tid < kpad) {
       const int kg = w0 + tid;
@@ -354,7 +353,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // SWIZZLE_128B (16-B chunk index XOR row index within each 1 KiB atom)
   auto stage = [&](const int *bb, int w0) {
     const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-    const int ktot = bb[4] < 0 ? 0 : e0 * e1 + e0 * e2 + e1 * e2 + hb;
+    const int ktot = e0 * e1 + e0 * e2 + e1 * e2 + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
     for (int e = tid; e < kpad * 8; e += 128) {
       const int kl = e >> 3, ch = e & 7;
@@ -371,6 +370,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
     if (patch >= npatch) break;
     PH(7);
     int v = 0, i = 0, j = 0;
+    int64_t r = 0;
     bool pix;
     Ray ray;
     ray.hit = false;
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       i = prow * kPatch + (slot >> 2);
       j = pcol * kPatch + (slot & 3);
-      const int64_t r = (int64_t)v * HW + (int64_t)i * P.W + j;
+      r = (int64_t)v * HW + (int64_t)i * P.W + j;
       pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
       if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
       if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
@@ -415,22 +415,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
       n_hit += alive ? 1 : 0;
     }
 
-    // Chunk pipeline (per group, chunk c = samples [k0, k0 + 8) of the 16 rays):
-    //   top:     wait for {blend(c), head(c-1)}; composite c-1 (head read from TMEM
-    //            columns kHeadCol..); rare extra blend windows of c
-    //   layers:  epilogue -> hidden layer MMAs of c (one round trip each); in the
-    //            first layer's MMA shadow the geometry, texel window, B staging and
-    //            sparse-A scatter of chunk c+1 are prepared (for the rays alive after
-    //            c-1's compositing: rays that terminate in c get one wasted chunk)
-    //   bottom:  ONE commit issues head(c) and blend(c+1): three MMA round trips per
-    //            chunk instead of four.
-    // The head writes its own 16 TMEM columns (kHeadCol), so blend(c+1) can overwrite
-    // the accumulator while head(c)'s result waits to be composited.
+    // Chunk pipeline: the geometry, texel window and cp.async staging of chunk
+    // c+1 are issued while chunk c's MLP runs on the tensor cores (the staged B
+    // tile is free once c's blend MMA has completed).  Chunk c+1 is prepared for
+    // the rays alive before c's compositing; rays that terminate in c get zero A
+    // rows in c+1.
+    int ix[3] = {0, 0, 0};
+    float wl[3] = {0.f, 0.f, 0.f}, wh[3] = {0.f, 0.f, 0.f};  // weights of texels ix, ix + 1
     int par = 0;
-    bool sv_n = false;  // this row's sample is valid in the prepared chunk
-    // a1-a3 for this row's sample of the chunk starting at kk: texel cell per axis
-    // (weights of texels ix, ix + 1)
-    auto geometry = [&](int kk, bool sv, int (&ix)[3], float (&wl)[3], float (&wh)[3]) {
+    // geometry + window + staging of window 0 for the chunk starting at kk (the
+    // chunk's bbox slot must still hold its reset state when this runs)
+    auto prefetch = [&](int kk, bool spec_alive) {
+      par = chunk_ctr & 1;
+      ++chunk_ctr;
+      const int k = kk + q;
+      // GRID: one point per row, z advancing 4 per chunk
+      const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : k < P.N);
       ix[0] = ix[1] = ix[2] = 0;
       wl[0] = wl[1] = wl[2] = 0.f;
       wh[0] = wh[1] = wh[2] = 0.f;
@@ -445,25 +445,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
             p[a] = __fadd_rn(P.lo[a], __fmul_rn(s, __fsub_rn(P.hi[a], P.lo[a])));
           }
         } else {
-          const int k = kk + q;
-          const float u = P.jitter ? jitter_u(P.seed, (uint64_t)(((int64_t)v * P.H + i) * P.W + j) * P.N + k)
-                                   : 0.5f;
+          const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
           sample_p(ray, sample_t(ray, delta, k, u), p);
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
           texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
       }
-    };
-    // geometry + window + staging of window 0 for the chunk starting at kk (the
-    // chunk's bbox slot must still hold its reset state when this runs)
-    auto prefetch = [&](int kk, bool spec_alive, int (&ix)[3], float (&wl)[3], float (&wh)[3]) {
-      par = chunk_ctr & 1;
-      ++chunk_ctr;
-      // GRID: one point per row, z advancing 4 per chunk
-      const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : kk + q < P.N);
-      sv_n = sv;
-      geometry(kk, sv, ix, wl, wh);
       int mn[3], mx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -482,61 +470,112 @@ __global__ void __launch_bounds__(128 * NG, 1)
       if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
       fill_table(sh->bbox[g][par], 0, true);
     };
-    // sparse-A rows of window [w0, w0 + kTcKMax) of the prepared chunk; returns kpad
-    auto scatter = [&](int w0, const int (&ix)[3], const float (&wl)[3], const float (&wh)[3]) -> int {
+
+    bool have = ptx::bar_red_or(bar_id, 128, alive);
+    if (have) prefetch(0, alive);
+    PH(0);
+    for (int k0 = 0; have;) {
+      const int k = k0 + q;
+      const int gz = gz0 + (k0 / kChunk) * 4;  // GRID: this chunk's z
+      const bool sv = alive && (GRID ? gz < P.grid_res : k < P.N);
       const int *bb = sh->bbox[g][par];
       const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
       const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
       // plane p uses axes (a, b): XY (0,1), XZ (0,2), YZ (1,2); row-major bbox rows
       const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
       const int ktex = base2 + ext1 * ext2;
-      const int ktot = bb[4] < 0 ? 0 : ktex + hb;  // empty window: no valid row
-      const int kp = min(kTcKMax, ktot - w0);
-      const int kpad = (kp + 15) & ~15;
-      for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
-      if (sv_n) {
-        const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
-        const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
-        const int bws[3] = {ext0, ext0, ext1};
-        const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
-        const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
+      const int ktot = ktex + hb;
+      const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
+      const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
+      const int bws[3] = {ext0, ext0, ext1};
+      const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
+      const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
+
+      // ---- blend on the tensor cores: window 0 was staged by prefetch; rare extra
+      //      windows (> kTcKMax texels) are staged synchronously
+      for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
+        const int kp = min(kTcKMax, ktot - w0);
+        const int kpad = (kp + 15) & ~15;
+        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
+        if (sv) {
 #pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-          const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
-          const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
-          const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
-          const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
+          for (int pl = 0; pl < 3; ++pl) {
+            const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
+            const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
+            const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
+            const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
+            for (int e = 0; e < 4; ++e)
+              if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
+          }
+          if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
+            ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);  // fp16 1.0: + b0
         }
-        if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
-          ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);  // fp16 1.0: + b0
+        if (w0 > 0) {  // synchronous staging of an extra window
+          fill_table(bb, w0, false);
+          ptx::bar_sync(bar_id, 128);
+          stage(bb, w0);
+        }
+        PH(1);
+        ptx::cp_async_wait_all();
+        ptx::fence_proxy_async_smem();
+        ptx::bar_sync(bar_id, 128);
+        if (tid == 0) {
+          ptx::tc_fence_after();
+          for (int ks = 0; ks < kpad / 16; ++ks) {
+            const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
+            const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
+            ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
+          }
+          ptx::mma_commit(&sh->mbar[g]);
+          sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
+          sh->n_kcols[g] += (unsigned)kpad;
+        }
+        ptx::mbar_wait(&sh->mbar[g], mphase);
+        mphase ^= 1u;
       }
-      return kpad;
-    };
-    auto window_total = [&]() {
-      const int *bb = sh->bbox[g][par];
-      const int e0 = bb[4] - bb[0] + 2, e1 = bb[5] - bb[1] + 2, e2 = bb[6] - bb[2] + 2;
-      return bb[4] < 0 ? 0 : e0 * e1 + e0 * e2 + e1 * e2 + hb;
-    };
-    // blend MMAs of one window (issuing thread only)
-    auto issue_blend = [&](int kpad, bool acc) {
-      for (int ks = 0; ks < kpad / 16; ++ks) {
-        const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
-        const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-        ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (acc || ks > 0) ? 1u : 0u);
+      ptx::tc_fence_after();
+      PH(2);
+
+      // ---- prefetch chunk c+1 (B tile is free), speculatively for the rays alive now
+      const int k1 = k0 + kChunk;
+      const bool nxt = GRID ? (k1 / kChunk < kGridKZ && gz0 - (tid >> 5) + (k1 / kChunk) * 4 < P.grid_res)
+                            : k1 < P.N;
+      if (nxt) prefetch(k1, alive);
+      PH(3);
+
+      // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
+      //      (A operand from TMEM), weights in shared memory
+      for (int l = 1; l < L; ++l) {
+        act_epilogue(tmem_row, tmem_row + kTcHD);
+        PH(4);
+        ptx::tc_fence_before();
+        ptx::bar_sync(bar_id, 128);
+        if (tid == 0) {
+          ptx::tc_fence_after();
+          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
+          const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
+          // the head skips its bias K block (4 FADDs at readout instead of an MMA)
+          const int nks = (l == L - 1) ? kTcHD / 16 : (int)kWK / 16;
+#pragma unroll
+          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
+            if (ks < nks) {
+              const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
+              ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
+            }
+          }
+          ptx::mma_commit(&sh->mbar[g]);
+        }
+        ptx::mbar_wait(&sh->mbar[g], mphase);
+        mphase ^= 1u;
+        ptx::tc_fence_after();
+        PH(5);
       }
-      sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
-      sh->n_kcols[g] += (unsigned)kpad;
-    };
-    // head readout + compositing (a4 head, a5) of the chunk starting at kc
-    auto head_composite = [&](int kc, bool svc) {
+      // ---- head: sigma, rgb (a4)
       uint32_t o4[4];
-      ptx::tmem_ld4(tmem_row + kHeadCol, o4);
+      ptx::tmem_ld4(tmem_row, o4);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      const bool sv = alive && svc;
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
         const float *bh = sh->head_bias;  // shared memory: broadcast reads
@@ -550,7 +589,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       if constexpr (GRID) {
         if (sv) {
-          const int gz = gz0 + (kc / kChunk) * 4;
           const int64_t n3 = (int64_t)P.grid_res * P.grid_res * P.grid_res;
           const int64_t rg = ((int64_t)gz * P.grid_res + gy) * P.grid_res + gx;
           P.grid_sigma[rg] = sigma;
@@ -560,9 +598,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
             P.grid_rgb[2 * n3 + rg] = c2;
           }
         }
-        return;
+        k0 = k1;
+        have = nxt;  // uniform over the group: no vote
+        continue;
       }
-      // a5: composite the ray's 8 samples (8-lane segmented scan)
+      // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
       const float tau = sv ? sigma * delta : 0.0f;
       float S = tau;
 #pragma unroll
@@ -578,140 +618,12 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const float Stot = __shfl_sync(0xffffffffu, S, kChunk - 1, kChunk);
       T = T * __expf(-Stot);
       if (alive && P.term_eps > 0.0f && T < P.term_eps) {
-        if (kc + kChunk < P.N && q == 0) n_term++;
+        if (nxt && q == 0) n_term++;
         alive = false;
       }
-    };
-    // is there a chunk after the one starting at kk (uniform over the group)
-    auto has_next = [&](int kk) {
-      const int k1 = kk + kChunk;
-      return GRID ? (k1 / kChunk < kGridKZ && gz0 - (tid >> 5) + (k1 / kChunk) * 4 < P.grid_res)
-                  : k1 < P.N;
-    };
-
-    bool have = ptx::bar_red_or(bar_id, 128, alive);
-    if (have) {
-      int ix[3];
-      float wl[3], wh[3];
-      prefetch(0, alive, ix, wl, wh);
-      const int kpad = scatter(0, ix, wl, wh);
-      ptx::cp_async_wait_all();
-      ptx::fence_proxy_async_smem();
-      ptx::bar_sync(bar_id, 128);
-      if (tid == 0) {
-        ptx::tc_fence_after();
-        issue_blend(kpad, false);
-        ptx::mma_commit(&sh->mbar[g]);
-      }
-    }
-    PH(0);
-    bool sv_prev = false;  // chunk k0 - 8's rows (its head is in flight when k0 > 0)
-    for (int k0 = 0; have;) {
-      const bool sv_c = sv_n;  // validity of chunk k0's rows (as prepared)
-      ptx::mbar_wait(&sh->mbar[g], mphase);
-      mphase ^= 1u;
-      ptx::tc_fence_after();
-      PH(2);
-      if (k0 > 0) head_composite(k0 - kChunk, sv_prev);
+      k0 = k1;
+      have = nxt && ptx::bar_red_or(bar_id, 128, alive);
       PH(6);
-      // ---- rare extra blend windows (> kTcKMax texels), staged synchronously
-      const int ktot = window_total();
-      for (int w0 = kTcKMax; w0 < ktot; w0 += kTcKMax) {
-        int ix[3];
-        float wl[3], wh[3];
-        geometry(k0, sv_c, ix, wl, wh);  // recomputed: not kept live across the layers
-        const int kpad = scatter(w0, ix, wl, wh);
-        fill_table(sh->bbox[g][par], w0, false);
-        ptx::bar_sync(bar_id, 128);
-        stage(sh->bbox[g][par], w0);
-        ptx::cp_async_wait_all();
-        ptx::fence_proxy_async_smem();
-        ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          issue_blend(kpad, true);
-          ptx::mma_commit(&sh->mbar[g]);
-        }
-        ptx::mbar_wait(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        ptx::tc_fence_after();
-      }
-      const bool nxt = has_next(k0);
-      bool prepared = false;
-      auto prepare_next = [&]() {  // chunk k0 + 8: geometry, window, staging, A rows
-        if (nxt) {
-          int ix[3];
-          float wl[3], wh[3];
-          prefetch(k0 + kChunk, alive, ix, wl, wh);
-          scatter(0, ix, wl, wh);
-        }
-        prepared = true;
-        PH(3);
-      };
-#ifndef DMV3D_PREP_AT
-#define DMV3D_PREP_AT 0  // 0: in layer 1's MMA shadow; 1: before, 2: after the first epilogue
-#endif
-      if (DMV3D_PREP_AT == 1) prepare_next();
-      // ---- hidden layers 1..L-2 on the tensor cores: fp16 activations live in TMEM
-      //      (A operand from TMEM), weights in shared memory
-      bool any = true;
-      for (int l = 1; l < L - 1; ++l) {
-        act_epilogue(tmem_row, tmem_row + kTcHD);
-        PH(4);
-        if (DMV3D_PREP_AT == 2 && l == 1) prepare_next();
-        ptx::tc_fence_before();
-        if (l == 1) {
-          any = ptx::bar_red_or(bar_id, 128, alive);  // every ray of the patch done?
-          if (!any) break;
-        } else {
-          ptx::bar_sync(bar_id, 128);
-        }
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
-#pragma unroll
-          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, idesc_hidden, ks > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&sh->mbar[g]);
-        }
-        if (DMV3D_PREP_AT == 0 && l == 1) prepare_next();
-        ptx::mbar_wait(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        ptx::tc_fence_after();
-        PH(5);
-      }
-      if (!any) break;
-      if (!prepared) prepare_next();  // L = 2: no hidden layer to hide it behind
-      // ---- head(c) and blend(c+1) in one commit
-      act_epilogue(tmem_row, tmem_row + kTcHD);
-      PH(4);
-      ptx::cp_async_wait_all();
-      ptx::fence_proxy_async_smem();
-      ptx::tc_fence_before();
-      const bool go = ptx::bar_red_or(bar_id, 128, nxt && alive);
-      if (tid == 0) {
-        ptx::tc_fence_after();
-        const uint32_t wbase = sW + (uint32_t)((L - 2) * kWHidden);
-        // the head skips its bias K block (4 FADDs at readout instead of an MMA)
-#pragma unroll
-        for (int ks = 0; ks < kTcHD / 16; ++ks) {
-          const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-          ptx::mma_f16_ts(tmem + kHeadCol, tmem + kTcHD + ks * 8, bd, idesc_head, ks > 0 ? 1u : 0u);
-        }
-        if (go) issue_blend(min(kTcKMax, (window_total() + 15) & ~15), false);
-        ptx::mma_commit(&sh->mbar[g]);
-      }
-      sv_prev = sv_c;
-      k0 += kChunk;
-      if (!go) {  // last chunk of the patch: composite it now
-        ptx::mbar_wait(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        ptx::tc_fence_after();
-        head_composite(k0 - kChunk, sv_prev);
-        break;
-      }
     }
     ptx::cp_async_wait_all();  // a prefetch for a chunk nobody needs may still be landing
     // ---- ray epilogue: reduce the 8 lanes, write rgb/alpha (+ DDIM x_{t-1})
