@@ -197,6 +197,9 @@ typedef struct {
                               element e of x_t gets Box-Muller of splitmix64(seed,
                               2e+1), splitmix64(seed, 2e+2) (24-bit uniforms)        */
   uint64_t noise_seed;
+  int32_t skip_kept_views; /* fused steps: 1 = views with keep_mask set are NOT rendered
+                              (their rgb / alpha are left untouched; x_{t-1} = x_t is
+                              written); 0 = they are rendered like any other view     */
 } dmv3d_ddim_params;
 
 /* ---------------------------------------------------------------- renderer */
@@ -216,13 +219,38 @@ dmv3d_status dmv3d_ddim_step(const dmv3d_ddim_params *params, int32_t V, int32_t
 /* One denoising step, fused: render all views of `cams` and, for the first
  * ddim_views views, apply the DDIM update in the per-ray epilogue.
  * x_t, z (NULL iff eta == 0), x_prev: [ddim_views][3][H][W].
- * rgb [V][3][H][W] and alpha [V][H][W] may each be NULL; when rgb is NULL the
- * views >= ddim_views are rendered for nothing, so pass V == ddim_views. */
+ * rgb [V][3][H][W] and alpha [V][H][W] may each be NULL; when BOTH are NULL only the
+ * views [0, ddim_views) are rendered (the others have no output to write). */
 dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_cameras *cams,
                                     const dmv3d_mlp *mlp, const dmv3d_render_opts *opts,
                                     const dmv3d_ddim_params *ddim, const float *x_t,
                                     const float *z, float *x_prev, float *rgb, float *alpha,
                                     dmv3d_stream stream);
+
+/* Batched assets (cfg4: PAPER.md:2538 trains/samples with 8 assets per GPU): one
+ * launch renders num_assets assets that share the MLP and (V, H, W), assets as the
+ * outer dimension of the work queue.  Every per-asset tensor gains a leading asset
+ * dimension, contiguous: triplane->data [A][3][R][R][C], cams->intrinsics [A][V][4],
+ * cams->c2w [A][V][3][4] (cams->num_views = V per asset), rgb [A][V][3][H][W], alpha
+ * [A][V][H][W], x_t / z / x_prev [A][ddim_views][3][H][W]; keep_mask [ddim_views]
+ * applies to every asset; opts ray ranges and tiles count global views a*V + v (ray
+ * id r = ((a V + v) H + i) W + j), and in-kernel noise uses the element index of the
+ * batched x_t.  The TCGEN05 engine needs dmv3d_workspace_bytes_batched() bytes (one
+ * projected triplane per asset).  Bitwise equal, asset by asset, to single-asset calls. */
+dmv3d_status dmv3d_render_views_batched(const dmv3d_triplane *triplane, int32_t num_assets,
+                                        const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                        const dmv3d_render_opts *opts, float *rgb, float *alpha,
+                                        dmv3d_stream stream);
+dmv3d_status dmv3d_render_ddim_step_batched(const dmv3d_triplane *triplane, int32_t num_assets,
+                                            const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                            const dmv3d_render_opts *opts,
+                                            const dmv3d_ddim_params *ddim, const float *x_t,
+                                            const float *z, float *x_prev, float *rgb,
+                                            float *alpha, dmv3d_stream stream);
+/* Render-only scratch of the TCGEN05 engine for num_assets assets (0 if it cannot run
+ * them); num_assets == 1 returns dmv3d_workspace_bytes(). */
+uint64_t dmv3d_workspace_bytes_batched(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                       int32_t num_assets);
 
 /* Plucker ray map: r = (o x d, d) per pixel, "concatenated with
  * image pixels" as the denoiser's camera conditioning, with o,

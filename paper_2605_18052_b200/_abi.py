@@ -26,6 +26,7 @@ EXPORTED = [
     "dmv3d_debug_sample_features", "dmv3d_debug_decode", "dmv3d_workspace_bytes",
     "dmv3d_timer_create", "dmv3d_timer_destroy", "dmv3d_timer_reset", "dmv3d_timer_read",
     "dmv3d_plucker_rays", "dmv3d_density_grid", "dmv3d_render_backward",
+    "dmv3d_render_views_batched", "dmv3d_render_ddim_step_batched", "dmv3d_workspace_bytes_batched",
 ]
 
 
@@ -64,7 +65,7 @@ class DdimParams(ct.Structure):
                 ("t_prev", ct.c_int32), ("eta", ct.c_float), ("x0_scale", ct.c_float),
                 ("x0_shift", ct.c_float), ("keep_mask", ct.POINTER(ct.c_uint8)),
                 ("ddim_views", ct.c_int32), ("noise_in_kernel", ct.c_int32),
-                ("noise_seed", ct.c_uint64)]
+                ("noise_seed", ct.c_uint64), ("skip_kept_views", ct.c_int32)]
 
 
 class DMV3DError(RuntimeError):
@@ -94,6 +95,15 @@ def lib() -> ct.CDLL:
         L.dmv3d_render_ddim_step.argtypes = [P(Triplane), P(Cameras), P(MLP), P(RenderOpts),
                                              P(DdimParams), ct.c_void_p, ct.c_void_p,
                                              ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]
+        L.dmv3d_render_views_batched.argtypes = [P(Triplane), ct.c_int32, P(Cameras), P(MLP),
+                                                 P(RenderOpts), ct.c_void_p, ct.c_void_p,
+                                                 ct.c_void_p]
+        L.dmv3d_render_ddim_step_batched.argtypes = [P(Triplane), ct.c_int32, P(Cameras), P(MLP),
+                                                     P(RenderOpts), P(DdimParams), ct.c_void_p,
+                                                     ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                                     ct.c_void_p, ct.c_void_p]
+        L.dmv3d_workspace_bytes_batched.argtypes = [P(Triplane), P(MLP), ct.c_int32]
+        L.dmv3d_workspace_bytes_batched.restype = ct.c_uint64
         L.dmv3d_workspace_create.argtypes = [P(ct.c_void_p)]
         L.dmv3d_workspace_destroy.argtypes = [ct.c_void_p]
         L.dmv3d_render_ddim_step_host.argtypes = [ct.c_void_p, P(Triplane), P(Cameras), P(MLP),
@@ -123,7 +133,8 @@ def lib() -> ct.CDLL:
         L.dmv3d_workspace_bytes.argtypes = [P(Triplane), P(MLP)]
         L.dmv3d_workspace_bytes.restype = ct.c_uint64
         for name in EXPORTED:
-            if name not in ("dmv3d_last_error", "dmv3d_version", "dmv3d_workspace_bytes"):
+            if name not in ("dmv3d_last_error", "dmv3d_version", "dmv3d_workspace_bytes",
+                            "dmv3d_workspace_bytes_batched"):
                 getattr(L, name).restype = ct.c_int
         _lib = L
     return _lib

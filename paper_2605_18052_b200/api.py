@@ -61,7 +61,10 @@ class DeviceMLP:
 
 def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0, 1.0, 1.0),
                     sample_mode="align_corners", fp8_scale=1.0):
-    """`tp` float32 / bfloat16 / float8_e4m3fn (value = fp8_scale * e4m3, TCGEN05 only)."""
+    """`tp` float32 / bfloat16 / float8_e4m3fn (value = fp8_scale * e4m3, TCGEN05 only);
+    [3,R,R,C], or [A,3,R,R,C] for the batched entry points."""
+    if tp.dim() == 5:
+        tp = tp[0]
     assert tp.dim() == 4 and tp.shape[0] == 3 and tp.shape[1] == tp.shape[2] and tp.is_contiguous()
     dt = {torch.float32: _abi.F32, torch.bfloat16: _abi.BF16,
           torch.float8_e4m3fn: _abi.FP8_E4M3}[tp.dtype]
@@ -71,9 +74,10 @@ def triplane_struct(tp: torch.Tensor, aabb_min=(-1.0, -1.0, -1.0), aabb_max=(1.0
 
 
 def cameras_struct(intrinsics: torch.Tensor, c2w: torch.Tensor, height: int, width: int):
+    """[V,4] / [V,3,4], or [A,V,4] / [A,V,3,4] for the batched entry points (V per asset)."""
     assert intrinsics.dtype == torch.float32 and c2w.dtype == torch.float32
     assert intrinsics.is_contiguous() and c2w.is_contiguous()
-    return _abi.Cameras(int(c2w.shape[0]), height, width, intrinsics.data_ptr(), c2w.data_ptr())
+    return _abi.Cameras(int(c2w.shape[-3]), height, width, intrinsics.data_ptr(), c2w.data_ptr())
 
 
 def opts_struct(samples_per_ray=128, agg="mean", jitter=False, seed=0, bg=(1.0, 1.0, 1.0),
@@ -198,10 +202,11 @@ class Timer:
 _WS_CACHE = {}
 
 
-def workspace_for(triplane_s, mlp_s, device, stream=None):
-    """Device scratch for the tensor-core engine (dmv3d_workspace_bytes), cached per
-    (device, stream): calls that share a workspace must be ordered on one stream."""
-    n = int(_abi.lib().dmv3d_workspace_bytes(ct.byref(triplane_s), ct.byref(mlp_s)))
+def workspace_for(triplane_s, mlp_s, device, stream=None, assets=1):
+    """Device scratch for the tensor-core engine (dmv3d_workspace_bytes[_batched]), cached
+    per (device, stream): calls that share a workspace must be ordered on one stream."""
+    n = int(_abi.lib().dmv3d_workspace_bytes_batched(ct.byref(triplane_s), ct.byref(mlp_s),
+                                                     int(assets)))
     if n == 0 or device.type != "cuda":
         return None
     key = (device.index, None if stream is None else stream.cuda_stream)
@@ -213,7 +218,7 @@ def workspace_for(triplane_s, mlp_s, device, stream=None):
 
 
 def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mask, ddim_views,
-                keep, x0_scale=2.0, x0_shift=-1.0, noise_seed=None):
+                keep, x0_scale=2.0, x0_shift=-1.0, noise_seed=None, skip_kept_views=False):
     ab = np.ascontiguousarray(alpha_bar, dtype=np.float64)
     keep.append(ab)
     km = None
@@ -224,7 +229,7 @@ def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mas
                            x0_scale, x0_shift,
                            km.ctypes.data_as(ct.POINTER(ct.c_uint8)) if km is not None else None,
                            ddim_views, 0 if noise_seed is None else 1,
-                           0 if noise_seed is None else int(noise_seed))
+                           0 if noise_seed is None else int(noise_seed), 1 if skip_kept_views else 0)
 
 
 # ------------------------------------------------------------------- entry points
@@ -268,8 +273,10 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
                            t, t_prev, x_t, z=None, eta=0.0, keep_mask=None, x_prev=None,
                            rgb=None, alpha=None, want_rgb=True, want_alpha=True,
                            aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3, x0_scale=2.0,
-                           x0_shift=-1.0, noise_seed=None, **opts):
-    """Fused step: render all views; views [0, x_t.shape[0]) also get x_{t-1}."""
+                           x0_shift=-1.0, noise_seed=None, skip_kept_views=False, **opts):
+    """Fused step: render all views; views [0, x_t.shape[0]) also get x_{t-1}.  With
+    want_rgb = want_alpha = False only those views are rendered; skip_kept_views: views
+    with keep_mask set are not rendered (x_{t-1} = x_t, their rgb/alpha untouched)."""
     V = int(c2w.shape[0])
     dv = int(x_t.shape[0])
     dev = triplane.device
@@ -287,12 +294,74 @@ def dmv3d_render_ddim_step(triplane, intrinsics, c2w, height, width, mlp: Device
     if "workspace" not in opts:
         opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev))
     o = opts_struct(**opts)
-    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift, noise_seed)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift, noise_seed,
+                    skip_kept_views)
     _abi.check(_abi.lib().dmv3d_render_ddim_step(ct.byref(tt), ct.byref(c), ct.byref(m),
                                                  ct.byref(o), ct.byref(d), _ptr(x_t), _ptr(z),
                                                  _ptr(x_prev), _ptr(rgb), _ptr(alpha),
                                                  _stream(dev)))
     return x_prev, rgb, alpha
+
+
+def dmv3d_render_ddim_step_batched(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
+                                   alpha_bar, t, t_prev, x_t, z=None, eta=0.0, keep_mask=None,
+                                   x_prev=None, rgb=None, alpha=None, want_rgb=True,
+                                   want_alpha=True, aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3,
+                                   x0_scale=2.0, x0_shift=-1.0, noise_seed=None,
+                                   skip_kept_views=False, **opts):
+    """Batched fused step (one launch for A assets sharing the MLP, cfg4): triplane
+    [A,3,R,R,C], intrinsics [A,V,4], c2w [A,V,3,4], x_t [A,DV,3,H,W] ->
+    (x_prev [A,DV,3,H,W], rgb [A,V,3,H,W], alpha [A,V,H,W])."""
+    A, V = int(c2w.shape[0]), int(c2w.shape[1])
+    dv = int(x_t.shape[1])
+    dev = triplane.device
+    assert triplane.dim() == 5 and triplane.shape[0] == A and x_t.shape[0] == A
+    if x_prev is None:
+        x_prev = torch.empty_like(x_t)
+    if rgb is None and want_rgb:
+        rgb = torch.empty((A, V, 3, height, width), device=dev, dtype=torch.float32)
+    if alpha is None and want_alpha:
+        alpha = torch.empty((A, V, height, width), device=dev, dtype=torch.float32)
+    keep = []
+    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                         fp8_scale=opts.pop("fp8_scale", 1.0))
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    if "workspace" not in opts:
+        opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev), assets=A)
+    o = opts_struct(**opts)
+    d = ddim_struct(alpha_bar, t, t_prev, eta, keep_mask, dv, keep, x0_scale, x0_shift, noise_seed,
+                    skip_kept_views)
+    _abi.check(_abi.lib().dmv3d_render_ddim_step_batched(ct.byref(tt), A, ct.byref(c), ct.byref(m),
+                                                         ct.byref(o), ct.byref(d), _ptr(x_t),
+                                                         _ptr(z), _ptr(x_prev), _ptr(rgb),
+                                                         _ptr(alpha), _stream(dev)))
+    return x_prev, rgb, alpha
+
+
+def dmv3d_render_views_batched(triplane, intrinsics, c2w, height, width, mlp: DeviceMLP,
+                               rgb=None, alpha=None, aabb_min=(-1.0,) * 3, aabb_max=(1.0,) * 3,
+                               **opts):
+    """Batched R(S, c): triplane [A,3,R,R,C], cameras [A,V,...] -> rgb [A,V,3,H,W],
+    alpha [A,V,H,W]."""
+    A, V = int(c2w.shape[0]), int(c2w.shape[1])
+    dev = triplane.device
+    if rgb is None:
+        rgb = torch.empty((A, V, 3, height, width), device=dev, dtype=torch.float32)
+    if alpha is None:
+        alpha = torch.empty((A, V, height, width), device=dev, dtype=torch.float32)
+    keep = []
+    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                         fp8_scale=opts.pop("fp8_scale", 1.0))
+    c = cameras_struct(intrinsics, c2w, height, width)
+    m = mlp.struct(keep)
+    if "workspace" not in opts:
+        opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev), assets=A)
+    o = opts_struct(**opts)
+    _abi.check(_abi.lib().dmv3d_render_views_batched(ct.byref(tt), A, ct.byref(c), ct.byref(m),
+                                                     ct.byref(o), _ptr(rgb), _ptr(alpha),
+                                                     _stream(dev)))
+    return rgb, alpha
 
 
 class Workspace:

@@ -149,6 +149,7 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
                  const dmv3d_mlp *m, const dmv3d_render_opts *o) {
   memset(&P, 0, sizeof(P));
   P.V = c->num_views;
+  P.V_asset = c->num_views;
   P.H = c->height;
   P.W = c->width;
   P.intr = c->intrinsics;
@@ -241,11 +242,11 @@ dmv3d_status ddim_coefficients(const dmv3d_ddim_params *d, int32_t nviews, DdimC
 enum class Engine { SIMT, TC };
 
 dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3d_render_opts *o,
-                         Engine &e) {
+                         Engine &e, int assets = 1) {
   const bool bf16 = (t->dtype == DMV3D_BF16 || t->dtype == DMV3D_FP8_E4M3) && m->dtype == DMV3D_BF16;
   const bool tc_ok = bf16 && m->hidden_act == DMV3D_ACT_RELU &&
                      tc_supported(t->channels, m->hidden, m->num_layers);
-  const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden);
+  const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden, assets);
   if (o->engine == DMV3D_ENGINE_TCGEN05) {
     if (!tc_ok)
       return fail(DMV3D_ERR_UNSUPPORTED,
@@ -279,17 +280,22 @@ dmv3d_status cuda_status(cudaError_t e, const char *what) {
 dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const dmv3d_mlp *m,
                          const dmv3d_render_opts *o, const dmv3d_ddim_params *d, const float *x_t,
                          const float *z, float *x_prev, float *rgb, float *alpha,
-                         cudaStream_t st, bool reuse_g = false) {
+                         cudaStream_t st, bool reuse_g = false, int assets = 1) {
   dmv3d_status s;
   if ((s = check_cams(c)) != DMV3D_OK) return s;
   if ((s = check_triplane(t)) != DMV3D_OK) return s;
-  const int64_t nrays = (int64_t)c->num_views * c->height * c->width;
+  CHECK_ARG(assets >= 1 && (int64_t)assets * c->num_views < (int64_t(1) << 31),
+            "batched: need 1 <= num_assets and num_assets * V < 2^31");
+  const int64_t nrays = (int64_t)assets * c->num_views * c->height * c->width;
+  CHECK_ARG(nrays < (int64_t(1) << 40), "too many rays");
   if ((s = check_opts(o, nrays)) != DMV3D_OK) return s;
   if ((s = check_mlp(m, t, o->agg)) != DMV3D_OK) return s;
   if (rgb) CHECK_ALIGN(rgb, "rgb");
   if (alpha) CHECK_ALIGN(alpha, "alpha");
   RenderParams P;
   fill_common(P, t, c, m, o);
+  P.V = assets * c->num_views;  // batched: assets x V views, asset-major
+  P.ray_end = (o->ray_begin == -1 && o->ray_end == -1) ? nrays : o->ray_end;
   P.rgb = rgb;
   P.alpha = alpha;
   P.reuse_g = reuse_g ? 1 : 0;
@@ -317,11 +323,17 @@ dmv3d_status render_impl(const dmv3d_triplane *t, const dmv3d_cameras *c, const 
     P.sqrt_ab_p = k.sqrt_ab_p;
     P.c_eps = k.c_eps;
     P.sigma_t = k.sigma_t;
+    // rays nobody needs: views >= ddim_views when neither rgb nor alpha is asked for,
+    // and (opt-in) kept conditioning views, whose x_{t-1} is x_t
+    P.ddim_only = (rgb == nullptr && alpha == nullptr) ? 1 : 0;
+    P.skip_kept = (d->skip_kept_views && k.keep_bits) ? 1 : 0;
   } else {
     CHECK_ARG(rgb != nullptr, "rgb is NULL");
   }
   Engine e;
-  if ((s = pick_engine(t, m, o, e)) != DMV3D_OK) return s;
+  if ((s = pick_engine(t, m, o, e, assets)) != DMV3D_OK) return s;
+  if (assets > 1 && e == Engine::SIMT && t->dtype == DMV3D_FP8_E4M3)
+    return fail(DMV3D_ERR_UNSUPPORTED, "fp8 triplane storage needs engine TCGEN05");
   cudaError_t ce;
   if (e == Engine::TC)
     ce = launch_render_tc(P, st);
@@ -553,6 +565,35 @@ dmv3d_status dmv3d_render_ddim_step(const dmv3d_triplane *triplane, const dmv3d_
   if (!ddim) return fail(DMV3D_ERR_INVALID_ARG, "ddim params is NULL");
   return render_impl(triplane, cams, mlp, opts, ddim, x_t, z, x_prev, rgb, alpha,
                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+dmv3d_status dmv3d_render_views_batched(const dmv3d_triplane *triplane, int32_t num_assets,
+                                        const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                        const dmv3d_render_opts *opts, float *rgb, float *alpha,
+                                        dmv3d_stream stream) {
+  g_err.clear();
+  return render_impl(triplane, cams, mlp, opts, nullptr, nullptr, nullptr, nullptr, rgb, alpha,
+                     reinterpret_cast<cudaStream_t>(stream), false, num_assets);
+}
+
+dmv3d_status dmv3d_render_ddim_step_batched(const dmv3d_triplane *triplane, int32_t num_assets,
+                                            const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
+                                            const dmv3d_render_opts *opts,
+                                            const dmv3d_ddim_params *ddim, const float *x_t,
+                                            const float *z, float *x_prev, float *rgb,
+                                            float *alpha, dmv3d_stream stream) {
+  g_err.clear();
+  if (!ddim) return fail(DMV3D_ERR_INVALID_ARG, "ddim params is NULL");
+  return render_impl(triplane, cams, mlp, opts, ddim, x_t, z, x_prev, rgb, alpha,
+                     reinterpret_cast<cudaStream_t>(stream), false, num_assets);
+}
+
+uint64_t dmv3d_workspace_bytes_batched(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                       int32_t num_assets) {
+  if (!triplane || !mlp || triplane->res < 2 || num_assets < 1) return 0;
+  if (!tc_supported(triplane->channels, mlp->hidden, mlp->num_layers)) return 0;
+  if (num_assets == 1) return dmv3d_workspace_bytes(triplane, mlp);
+  return tc_workspace_bytes(triplane->res, mlp->hidden, num_assets);
 }
 
 dmv3d_status dmv3d_ddim_step(const dmv3d_ddim_params *params, int32_t V, int32_t H, int32_t W,

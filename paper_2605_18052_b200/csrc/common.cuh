@@ -19,8 +19,10 @@ constexpr int kMaxPeers = 7;  // the other GPUs of an 8-GPU node
 
 // All per-launch parameters; passed by value as a __grid_constant__.
 struct RenderParams {
-  // camera set C
+  // camera set C; a batched launch renders `V / V_asset` assets of
+  // V_asset views each (global view v = asset * V_asset + local view)
   int32_t V, H, W;
+  int32_t V_asset;
   const float *intr;  // [V][4]
   const float *c2w;   // [V][3][4]
   // triplane S
@@ -53,6 +55,8 @@ struct RenderParams {
   float *x_prev;
   float x0_scale, x0_shift;
   float sqrt_ab_t, inv_sqrt_1m_ab_t, sqrt_ab_p, c_eps, sigma_t;
+  int32_t ddim_only;  // fused step without rgb/alpha: views >= ddim_views are not rendered
+  int32_t skip_kept;  // kept views (keep_bits) are not rendered: x_{t-1} = x_t copied
   uint64_t noise_seed;  // z == null && sigma_t != 0: in-kernel noise (row f4)
   unsigned long long *counters;
   // caller-owned scratch (tensor-core engine: patch counter + projected triplane)
@@ -319,9 +323,35 @@ static __device__ __noinline__ void peer_store_xp(const RenderParams &P, int64_t
     if (P.peer_xp[k]) P.peer_xp[k][idx] = xp;
 }
 
+__device__ __forceinline__ bool kept_view(const RenderParams &P, int vl) {
+  return vl < 64 && ((P.keep_bits >> vl) & 1ull);
+}
+
+// What a fused step does with the rays of global view v: 0 = render, 1 = nothing
+// (ddim_only: a view >= ddim_views whose rgb/alpha nobody asked for), 2 = copy x_t into
+// x_{t-1} without rendering (skip_kept: a kept conditioning view).
+__device__ __forceinline__ int view_action(const RenderParams &P, int v) {
+  if (!P.ddim_only && !P.skip_kept) return 0;
+  const int vl = v % P.V_asset;
+  if (P.ddim_only && vl >= P.ddim_views) return 1;
+  if (P.skip_kept && vl < P.ddim_views && kept_view(P, vl)) return 2;
+  return 0;
+}
+// x_{t-1} = x_t for channel ch of pixel (i, j) of a kept view (view_action == 2)
+__device__ __forceinline__ void copy_kept(const RenderParams &P, int v, int i, int j, int ch) {
+  const int64_t HW = (int64_t)P.H * P.W;
+  const int a = v / P.V_asset, vl = v - a * P.V_asset;
+  const int64_t idx = (((int64_t)a * P.ddim_views + vl) * 3 + ch) * HW + (int64_t)i * P.W + j;
+  const float xt = __ldg(P.x_t + idx);
+  P.x_prev[idx] = xt;
+  if (P.npeers) peer_store_xp(P, idx, xt);
+}
+
 // Per-ray epilogue: write rgb/alpha and, for DDIM views, x_{t-1}
 // (readings A15, A18-A20).  `ch` selects the channel this
-// thread writes (0..2); channel 0's thread also writes alpha.
+// thread writes (0..2); channel 0's thread also writes alpha.  Batched launches:
+// view v is local view v % V_asset of asset v / V_asset; x_t / z / x_{t-1} are
+// [assets][ddim_views][3][H][W].
 __device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i, int j, int ch,
                                              float c_val, float T) {
   const int64_t HW = (int64_t)P.H * P.W;
@@ -331,11 +361,12 @@ __device__ __forceinline__ void ray_epilogue(const RenderParams &P, int v, int i
   if (P.rgb) P.rgb[irgb] = out;
   if (ch == 0 && P.alpha) P.alpha[ia] = 1.0f - T;
   if (P.npeers) peer_store_rgb(P, irgb, ia, ch, out, 1.0f - T);
-  if (v < P.ddim_views) {
-    const int64_t idx = ((int64_t)v * 3 + ch) * HW + pix;
+  const int a = v / P.V_asset, vl = v - a * P.V_asset;
+  if (vl < P.ddim_views) {
+    const int64_t idx = (((int64_t)a * P.ddim_views + vl) * 3 + ch) * HW + pix;
     const float xt = __ldg(P.x_t + idx);
     float xp;
-    if ((P.keep_bits >> v) & 1ull) {
+    if (kept_view(P, vl)) {
       xp = xt;
     } else {
       const float x0 = P.x0_scale * out + P.x0_shift;

@@ -24,7 +24,7 @@ __global__ void ddim_kernel(const __grid_constant__ DdimCoef c, int64_t per_view
        q += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)((q * 4) / per_view);
     const float4 xt = __ldg(x_t + q);
-    if ((c.keep_bits >> v) & 1ull) {
+    if (v < 64 && ((c.keep_bits >> v) & 1ull)) {  // keep_mask covers <= 64 views
       out[q] = xt;
       continue;
     }
@@ -58,7 +58,7 @@ __global__ void ddim_kernel_scalar(const __grid_constant__ DdimCoef c, int64_t p
     const int v = (int)(q / per_view);
     const float xt = x_t[q];
     const float zq = c.sigma_t == 0.0f ? 0.0f : (z ? z[q] : ddim_noise(c.noise_seed, (uint64_t)q));
-    out[q] = ((c.keep_bits >> v) & 1ull) ? xt : ddim_one(c, xt, x0[q], zq);
+    out[q] = (v < 64 && ((c.keep_bits >> v) & 1ull)) ? xt : ddim_one(c, xt, x0[q], zq);
   }
 }
 

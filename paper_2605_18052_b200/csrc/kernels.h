@@ -42,7 +42,7 @@ cudaError_t launch_render_backward(const RenderParams &P, const GradParams &Gp, 
 // [G: (3 R R + 1) x HD fp16] (+ for the backward, 256-B aligned: [dG: (3 R R + 1) x HD fp32])
 constexpr uint32_t kTcWsHeader = 256;
 bool tc_supported(int C, int HD, int L);  // C = triplane channels per plane
-size_t tc_workspace_bytes(int R, int HD);
+size_t tc_workspace_bytes(int R, int HD, int assets = 1);  // render: header + assets x G
 cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st);
 cudaError_t launch_render_tc(const RenderParams &P, cudaStream_t st);
 

@@ -34,9 +34,16 @@ __global__ void __launch_bounds__(kSimtThreads)
     ray_pixel(r, P.H, P.W, v, i, j);
     if (P.tile_size > 0 && tile_of(v, i, j, P.H, P.W, P.tile_size) % P.tile_count != P.tile_rank)
       continue;  // another rank's tile
+    const int act = view_action(P, v);
+    if (act != 0) {  // not rendered: nothing, or x_{t-1} = x_t for a kept view
+      if (act == 2 && lane < 3) copy_kept(P, v, i, j, lane);
+      continue;
+    }
     const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
     if (P.plucker && lane < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, lane, ray);
     n_rays++;
+    // batched launch: this view's asset owns the triplane at element offset asset * 3 R R C
+    const int64_t tp_off = (int64_t)(v / P.V_asset) * 3 * P.R * P.R * P.C;
     if (!ray.hit) {
       if (lane < 3) ray_epilogue(P, v, i, j, lane, 0.0f, 1.0f);
       continue;
@@ -54,7 +61,7 @@ __global__ void __launch_bounds__(kSimtThreads)
         float p[3];
         sample_p(ray, sample_t(ray, delta, k, u), p);
         float x[K];
-        gather_features<BF16, K, CAT>(P, p, x);
+        gather_features<BF16, K, CAT>(P, p, x, tp_off);
         mlp_decode<K, HD>(P, m, x, my_act, blockDim.x, sigma, c);
       }
       // a5: front-to-back compositing as a warp prefix sum of optical depth

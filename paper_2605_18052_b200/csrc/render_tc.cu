@@ -75,7 +75,9 @@ constexpr size_t kSmemLimit = 232448;                  // 227 KiB per CTA
 
 // header (patch counter) + G [3 R R + 1][HD]: the last row holds b0 for the
 // half-pixel mode's bias column
-size_t tc_workspace_bytes(int R, int HD) { return kWsHeader + ((size_t)3 * R * R + 1) * HD * 2; }
+size_t tc_workspace_bytes(int R, int HD, int assets) {
+  return kWsHeader + (size_t)assets * ((size_t)3 * R * R + 1) * HD * 2;
+}
 
 // C = channels per plane (the MLP input is 3 C for the concat aggregation)
 bool tc_supported(int C, int HD, int L) {
@@ -111,15 +113,17 @@ __global__ void __launch_bounds__(256)
     preproject_kernel(const void *__restrict__ Fv, int ntex, int C, int wstride,
                       const __nv_bfloat16 *__restrict__ W0, const float *__restrict__ b0,
                       float bscale, float fscale, __half *__restrict__ G, unsigned int *counter,
-                      __half *__restrict__ gbias) {
+                      __half *__restrict__ gbias, int64_t per_asset, int assets) {
   extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
   for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {  // o fastest: conflict-free stores
     const int c = e / kTcHD, o = e - c * kTcHD;
     reinterpret_cast<float *>(swt)[c * kTcHD + o] = __bfloat162float(W0[(size_t)o * wstride + c]);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && counter) *counter = 0u;
-  if (blockIdx.x == 0 && gbias && threadIdx.x < kTcHD)
-    gbias[threadIdx.x] = __float2half_rn(__ldg(b0 + threadIdx.x));
+  if (blockIdx.x == 0 && gbias)  // every asset's bias row (G block row per_asset)
+    for (int e = threadIdx.x; e < assets * kTcHD; e += blockDim.x)
+      gbias[(int64_t)(e / kTcHD) * (per_asset + 1) * kTcHD + e % kTcHD] =
+          __float2half_rn(__ldg(b0 + e % kTcHD));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bias0 = __ldg(b0 + 2 * lane) * bscale, bias1 = __ldg(b0 + 2 * lane + 1) * bscale;
@@ -177,7 +181,8 @@ __global__ void __launch_bounds__(256)
       cur = nxt;
     }
     const uint32_t pk = (uint32_t)ptx::f32_to_f16(a0) | ((uint32_t)ptx::f32_to_f16(a1) << 16);
-    reinterpret_cast<uint32_t *>(G + t * kTcHD)[lane] = pk;
+    const int64_t ta = t / per_asset;  // asset: its G block has one extra (bias) row
+    reinterpret_cast<uint32_t *>(G + (t + ta) * kTcHD)[lane] = pk;
   }
 }
 
@@ -275,8 +280,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
   constexpr uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
   constexpr uint32_t idesc_head = ptx::idesc_f16(128, 16, 0);
 
-  const __half *G = reinterpret_cast<const __half *>(reinterpret_cast<const uint8_t *>(P.tp) +
-                                                      kWsHeader);
+  const __half *G0 = reinterpret_cast<const __half *>(reinterpret_cast<const uint8_t *>(P.tp) +
+                                                       kWsHeader);
+  const int64_t g_stride = ((int64_t)3 * P.R * P.R + 1) * kTcHD;  // per asset (batched launches)
+  const __half *G = G0;
   unsigned int *counter = reinterpret_cast<unsigned int *>(const_cast<void *>(P.tp));
 
   // patch space: views [v_lo, v_hi] of the ray range, 4x4 patches
@@ -402,6 +409,15 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       i = prow * kPatch + (slot >> 2);
       j = pcol * kPatch + (slot & 3);
+      G = G0 + (int64_t)(v / P.V_asset) * g_stride;  // this view's asset's projected triplane
+      const int act = view_action(P, v);               // uniform over the patch
+      if (act != 0) {  // not rendered: nothing, or x_{t-1} = x_t for a kept view
+        if (act == 2 && q < 3 && i < P.H && j < P.W) {
+          const int64_t rr = (int64_t)v * HW + (int64_t)i * P.W + j;
+          if (rr >= P.ray_begin && rr < P.ray_end) copy_kept(P, v, i, j, q);
+        }
+        continue;
+      }
       r = (int64_t)v * HW + (int64_t)i * P.W + j;
       pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
       if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
@@ -692,6 +708,7 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntex = 3 * P.R * P.R;
+  const int A = P.V / P.V_asset;  // assets of a batched launch (each its own G block)
   const size_t s0 = (size_t)kTcHD * P.C * 4;
   auto kern = P.tp_fp8 ? preproject_kernel<true> : preproject_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
@@ -701,20 +718,32 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   const size_t esz = P.tp_fp8 ? 1 : 2;
   const __nv_bfloat16 *W0 = reinterpret_cast<const __nv_bfloat16 *>(P.w[0]);
   const bool cat = P.agg == 2;
-  const int nlaunch = cat ? 3 : 1, nt = cat ? P.R * P.R : ntex;
 #ifndef DMV3D_K0_BLOCKS_PER_SM
 #define DMV3D_K0_BLOCKS_PER_SM 2  // fewer blocks: each loads W0 (20 KiB) once; 8 measured 1 % slower on cfg2
 #endif
+  const size_t gs = ((size_t)ntex + 1) * kTcHD;  // G block of one asset
+  if (!cat) {  // all assets' texels in one launch
+    const int64_t nt = (int64_t)A * ntex;
+    int64_t g0 = (nt * 32 + 255) / 256;
+    if (g0 > sms * DMV3D_K0_BLOCKS_PER_SM) g0 = sms * DMV3D_K0_BLOCKS_PER_SM;
+    kern<<<(int)g0, 256, s0, st>>>(F, (int)nt, P.C, P.C, W0, P.b[0], bscale, P.tp_scale, G, counter,
+                                   G + (size_t)ntex * kTcHD, ntex, A);
+    return cudaGetLastError();
+  }
+  // concat: plane p of every asset is projected by its own column block of W0
+  const int nt = P.R * P.R;
   int g0 = (nt * 32 + 255) / 256;
   if (g0 > sms * DMV3D_K0_BLOCKS_PER_SM) g0 = sms * DMV3D_K0_BLOCKS_PER_SM;
-  for (int pl = 0; pl < nlaunch; ++pl) {
-    kern<<<g0, 256, s0, st>>>(F + (size_t)pl * nt * P.C * esz, nt, P.C, cat ? 3 * P.C : P.C,
-                              W0 + (size_t)pl * P.C, P.b[0], bscale, P.tp_scale,
-                                           G + (size_t)pl * nt * kTcHD, pl == 0 ? counter : nullptr,
-                                           pl == 0 ? G + (size_t)ntex * kTcHD : nullptr);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
+  for (int a = 0; a < A; ++a)
+    for (int pl = 0; pl < 3; ++pl) {
+      const bool first = a == 0 && pl == 0;
+      kern<<<g0, 256, s0, st>>>(F + ((size_t)a * 3 + pl) * nt * P.C * esz, nt, P.C, 3 * P.C,
+                                W0 + (size_t)pl * P.C, P.b[0], bscale, P.tp_scale,
+                                G + a * gs + (size_t)pl * nt * kTcHD, first ? counter : nullptr,
+                                first ? G + (size_t)ntex * kTcHD : nullptr, ntex, first ? A : 0);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
   return cudaSuccess;
 }
 

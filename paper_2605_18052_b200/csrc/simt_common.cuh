@@ -12,7 +12,7 @@ namespace dmv3d {
 // fills x[pl C, (pl + 1) C), else K = C and the planes are summed (x 1/3: mean).
 template <bool BF16, int K, bool CAT = false>
 __device__ __forceinline__ void gather_features(const RenderParams &P, const float p[3],
-                                                float x[K]) {
+                                                float x[K], int64_t tp_off = 0) {
   constexpr int CP = CAT ? K / 3 : K;
 #pragma unroll
   for (int c = 0; c < K; ++c) x[c] = 0.0f;
@@ -24,7 +24,7 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
     float *xp = x + (CAT ? pl * CP : 0);
     const int64_t rowC = (int64_t)P.R * P.C;
     if constexpr (BF16) {
-      const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(P.tp) + cell.off;
+      const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(P.tp) + tp_off + cell.off;
       const uint4 *t00 = reinterpret_cast<const uint4 *>(base);
       const uint4 *t01 = reinterpret_cast<const uint4 *>(base + P.C);
       const uint4 *t10 = reinterpret_cast<const uint4 *>(base + rowC);
@@ -43,7 +43,7 @@ __device__ __forceinline__ void gather_features(const RenderParams &P, const flo
         }
       }
     } else {
-      const float *base = reinterpret_cast<const float *>(P.tp) + cell.off;
+      const float *base = reinterpret_cast<const float *>(P.tp) + tp_off + cell.off;
       const float4 *t00 = reinterpret_cast<const float4 *>(base);
       const float4 *t01 = reinterpret_cast<const float4 *>(base + P.C);
       const float4 *t10 = reinterpret_cast<const float4 *>(base + rowC);

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the sharding/merge logic in
 paper_2605_18052_b200.dist, with the CPU oracle standing in for the renderer:
-the gathered views equal one process rendering everything (bitwise), the
-triplane broadcast reaches every rank, and asset shards cover the batch."""
+the gathered views equal one process rendering everything (bitwise) -- also with
+the DDIM keep-mask and eta > 0, whose view indices must stay global on every rank --,
+the triplane broadcast reaches every rank, and asset shards cover the batch."""
 import os
 import socket
 
@@ -32,15 +33,21 @@ def _workload():
 
 
 def _oracle_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t_prev, x_t, x_prev, rgb,
-                      alpha, samples_per_ray=16):
+                      alpha, samples_per_ray=16, ray_range=None, eta=0.0, z=None, keep_mask=None):
+    """The oracle as the fused step over the FULL camera set, writing only the views of
+    `ray_range` (whole views), with the one-GPU step's DDIM arguments."""
     import oracle
     cams = wl.Cameras(intrinsics.numpy(), c2w.numpy(), H, W)
     orgb, oalpha = oracle.render_views(triplane.numpy(), cams, mlp, samples_per_ray, threads=1)
-    rgb.copy_(torch.from_numpy(orgb.astype(np.float32)))
-    alpha.copy_(torch.from_numpy(oalpha.astype(np.float32)))
+    V = orgb.shape[0]
+    v0, v1 = (0, V) if ray_range is None else (ray_range[0] // (H * W), ray_range[1] // (H * W))
+    rgb[v0:v1] = torch.from_numpy(orgb[v0:v1].astype(np.float32))
+    alpha[v0:v1] = torch.from_numpy(oalpha[v0:v1].astype(np.float32))
     if x_t is not None:
-        xp = oracle.ddim_step(alpha_bar, t, t_prev, x_t.numpy(), orgb[:x_t.shape[0]])
-        x_prev.copy_(torch.from_numpy(xp.astype(np.float32)))
+        dv = x_t.shape[0]
+        xp = oracle.ddim_step(alpha_bar, t, t_prev, x_t.numpy(), orgb[:dv], eta=eta,
+                              z=None if z is None else z.numpy(), keep_mask=keep_mask)
+        x_prev[v0:min(v1, dv)] = torch.from_numpy(xp[v0:min(v1, dv)].astype(np.float32))
 
 
 def _oracle_tile_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t_prev, x_t, x_prev,
@@ -105,7 +112,10 @@ def test_tile_owner_partition(H, W, T, P):
     assert owners[0, 0, 0] == 0 and (W > T) == (owners[0, 0, min(T, W - 1)] == 1 % P)
 
 
-def _worker(rank, world, port, out_dir):
+DDIM_KW = {"plain": {}, "keep_eta": {"eta": 1.0, "keep_mask": [0, 0, 1]}}
+
+
+def _worker(rank, world, port, out_dir, case="plain"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -114,9 +124,12 @@ def _worker(rank, world, port, out_dir):
         triplane = torch.from_numpy(tp) if rank == 0 else torch.zeros_like(torch.from_numpy(tp))
         ab = schedule.cosine_alpha_bar()
         x_t = torch.from_numpy(wl.gaussian((3, 3, 6, 5), 4))
+        kw = dict(DDIM_KW[case])
+        if kw.get("eta"):
+            kw["z"] = torch.from_numpy(wl.gaussian((3, 3, 6, 5), 9))
         xp, rgb, alpha = pdist.denoise_step_view_sharded(
             triplane, torch.from_numpy(cams.intrinsics), torch.from_numpy(cams.c2w), 6, 5, m, ab,
-            980, 960, x_t, ddim_views=3, render_fn=_oracle_render_fn, samples_per_ray=16)
+            980, 960, x_t, ddim_views=3, render_fn=_oracle_render_fn, samples_per_ray=16, **kw)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), xp=xp.numpy(), rgb=rgb.numpy(),
                  alpha=alpha.numpy(), tp=triplane.numpy(),
                  t=np.array([pdist.max_over_ranks(float(rank + 1), "cpu")]))
@@ -124,14 +137,20 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def test_view_sharded_step_matches_single_process(tmp_path):
+@pytest.mark.parametrize("case", ["plain", "keep_eta"])
+def test_view_sharded_step_matches_single_process(tmp_path, case):
+    """Rank 1 owns views 3-4: a novel view and the last DDIM view (which is the kept
+    one in "keep_eta"), so keep_mask / z / x_t must be read at global view indices."""
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world, join=True)
     import oracle
     tp, m, cams = _workload()
     orgb, oalpha = oracle.render_views(tp, cams, m, 16, threads=1)
     x_t = wl.gaussian((3, 3, 6, 5), 4)
-    oxp = oracle.ddim_step(schedule.cosine_alpha_bar(), 980, 960, x_t, orgb[:3])
+    kw = dict(DDIM_KW[case])
+    if kw.get("eta"):
+        kw["z"] = wl.gaussian((3, 3, 6, 5), 9)
+    oxp = oracle.ddim_step(schedule.cosine_alpha_bar(), 980, 960, x_t, orgb[:3], **kw)
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert np.array_equal(d["tp"], tp)  # broadcast from the owner rank
