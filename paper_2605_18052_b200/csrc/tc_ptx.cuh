@@ -48,6 +48,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// Plain arrive (count 1), release semantics at CTA scope: the caller's prior shared-memory
+// writes are visible to threads that observe the phase completion.
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// Warpgroup register re-balancing (all 4 warps of the warpgroup execute it).
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+// Shared-memory flag hand-off between warp roles (acquire load / release store).
+__device__ __forceinline__ uint32_t lds_acquire(const void *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_release(void *p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 // Bounded wait: traps (a launch error instead of a hung GPU) if the phase has not
 // completed after ~2^24 polls -- seconds, far beyond any legitimate wait here.
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t parity) {
