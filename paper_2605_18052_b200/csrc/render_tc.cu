@@ -31,10 +31,6 @@
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 
-#include <algorithm>
-#include <cstdlib>
-#include <cstring>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -687,607 +683,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
   }
 }
 
-// ------------------------------------------------------------------ K1, warp-specialised
-// render_ws_kernel: the same per-chunk
-// arithmetic as render_tc_kernel, with the work split by role so that a group's TMEM
-// tile turns over at the rate of its MMA chain instead of its whole chunk:
-//  * 4 MLP groups (warps 4g..4g+3, 128 TMEM lanes each): per staged tile, the blend
-//    MMA, the layer epilogues + MMAs, the head, the compositing and the ray epilogue.
-//    A group alternates between two patches ("slots"), so the tile it consumes next
-//    never depends on the compositing of the tile it is finishing;
-//  * 2 sampler warpgroups (warps 16..23), each feeding two groups: patch fetch, rays
-//    (a1), sample points and texel cells (a2-a3), the per-plane texel window, the
-//    cp.async staging of G and the sparse A rows -- into the group's single stage,
-//    handed over through mbarriers (full: staged; empty: the blend MMA has read it).
-//  The sampler stages slot x's next chunk for the rays the group marked alive when it
-//  composited x's previous chunk (no speculation).
-constexpr int kWsGroups = 4;
-constexpr int kWsSamplers = 2;
-constexpr int kWsThreads = 128 * (kWsGroups + kWsSamplers);
-constexpr int kWsSlots = 2 * kWsGroups;
-enum : int { kWsFirst = 1, kWsLast = 2, kWsWin0 = 4, kWsDone = 8 };
-
-#ifdef DMV3D_WS_DEBUG  // hand-off waits trap instead of hanging
-#define WS_WAIT(bar, par) ptx::mbar_wait_bounded(bar, par)
-#define WS_SPIN_CHECK(n) \
-  if ((n) > (1u << 26)) __trap()
-#else
-#define WS_WAIT(bar, par) ptx::mbar_wait(bar, par)
-#define WS_SPIN_CHECK(n)
-#endif
-
-struct WsRay {
-  float o[3], d[3], t_near, delta;
-};
-
-struct WsShared {
-  uint64_t full[kWsGroups], empty[kWsGroups], mbar[kWsGroups];
-  uint32_t tmem_base;
-  int desc[kWsGroups][4];  // staged window: slot (0/1), k0, kpad, flags
-  WsRay ray[kWsSlots][16];
-  // per-ray bit masks of a slot's patch: byte w holds rays 4w..4w+3 in bits 0..3
-  uint32_t slot_hit[kWsSlots];    // pix && hit (alive at the first chunk)
-  uint32_t slot_pix[kWsSlots];
-  uint32_t slot_alive[kWsSlots];  // rays that continue after the last composited chunk
-  int slot_v[kWsSlots], slot_i0[kWsSlots], slot_j0[kWsSlots];
-  uint32_t composited[kWsGroups];  // tiles composited by each group (release / acquire)
-  int bbox[kWsSamplers][2][8];
-  long long fetch[kWsSamplers];
-  float head_bias[4];
-  unsigned n_tiles[kWsGroups], n_kcols[kWsGroups];
-};
-
-static size_t ws_smem_bytes(int L) {
-  return 1024 + (size_t)kWsGroups * (kATileBytes + kBTileBytes) + (size_t)(L - 2) * kWHidden + kWHead +
-         sizeof(WsShared);
-}
-
-__device__ __forceinline__ bool ray_bit(uint32_t m, int s) { return (m >> (8 * (s >> 2) + (s & 3))) & 1u; }
-// this warp's 4 rays (lanes 0, 8, 16, 24) of a ballot -> the nibble of mask byte w
-__device__ __forceinline__ uint32_t ray_nibble(uint32_t b) {
-  return (b & 1u) | ((b >> 7) & 2u) | ((b >> 14) & 4u) | ((b >> 21) & 8u);
-}
-
-struct WsFeed {  // a sampler's bookkeeping for one group (uniform over the warpgroup)
-  int g;
-  uint32_t nwin;  // windows staged (full / empty phases)
-  int ntile;      // tiles staged
-  int last;       // slot of the last tile
-  int st0, st1;   // slot state: 0 needs a patch, 1 active, 2 dead
-  int k00, k01;   // next chunk of each slot
-  int ti0, ti1;   // index of each slot's last tile (-1: none)
-  bool done;
-};
-
-// Fetch the next renderable patch into `slot` (all 128 threads of sampler warpgroup k):
-// rays, Plucker map, view skipping, fully-missed patches written out directly.  False:
-// the queue is exhausted.  Out of line: once per patch, kept out of the hot loop's
-// instruction footprint.
-static __device__ __noinline__ void ws_ray_out(const RenderParams &P, int v, int i, int j, int ch,
-                                               float c_val, float T) {
-  ray_epilogue(P, v, i, j, ch, c_val, T);
-}
-
-struct WsQueue {
-  int64_t HW, npatch, tile_first, TH, TW;
-  int v_lo, PH, PW, TP;
-  unsigned int *counter;
-};
-static __device__ __noinline__ bool ws_fetch_patch(const RenderParams &P, WsShared *sh, const WsQueue &Q,
-                                                   int k, int tid, int slot, unsigned &n_rays,
-                                                   unsigned &n_hit) {
-  const int s = tid >> 3, q = tid & 7;
-  const int bar_id = 1 + kWsGroups + k;
-  const int64_t HW = Q.HW;
-  for (;;) {
-    if (tid == 0) sh->fetch[k] = (long long)atomicAdd(Q.counter, 1u);
-    ptx::bar_sync(bar_id, 128);
-    const int64_t patch = sh->fetch[k];
-    ptx::bar_sync(bar_id, 128);
-    if (patch >= Q.npatch) return false;
-    int v, prow, pcol;
-    if (Q.TP > 0) {
-      const int TP = Q.TP;
-      const int64_t tau = Q.tile_first + (patch / (TP * TP)) * P.tile_count;
-      const int w = (int)(patch % (TP * TP));
-      v = (int)(tau / (Q.TH * Q.TW));
-      const int64_t trem = tau % (Q.TH * Q.TW);
-      prow = (int)(trem / Q.TW) * TP + w / TP;
-      pcol = (int)(trem % Q.TW) * TP + w % TP;
-    } else {
-      v = Q.v_lo + (int)(patch / ((int64_t)Q.PH * Q.PW));
-      const int prem = (int)(patch % ((int64_t)Q.PH * Q.PW));
-      prow = prem / Q.PW;
-      pcol = prem % Q.PW;
-    }
-    const int i = prow * kPatch + (s >> 2), j = pcol * kPatch + (s & 3);
-    const int act = view_action(P, v);
-    if (act != 0) {
-      if (act == 2 && q < 3 && i < P.H && j < P.W) {
-        const int64_t rr = (int64_t)v * HW + (int64_t)i * P.W + j;
-        if (rr >= P.ray_begin && rr < P.ray_end) copy_kept(P, v, i, j, q);
-      }
-      continue;
-    }
-    const int64_t r = (int64_t)v * HW + (int64_t)i * P.W + j;
-    const bool pix = (i < P.H) && (j < P.W) && r >= P.ray_begin && r < P.ray_end;
-    Ray ray;
-    ray.hit = false;
-    ray.t_near = ray.t_far = 0.0f;
-    if (pix) ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
-    if (pix && P.plucker && q < 6) plucker_write(P.plucker, P.H, P.W, v, i, j, q, ray);
-    const bool hit = pix && ray.hit;
-    if (q == 0) {
-      n_rays += pix ? 1 : 0;
-      n_hit += hit ? 1 : 0;
-    }
-    if (!ptx::bar_red_or(bar_id, 128, hit)) {
-      if (pix && q < 3) ray_epilogue(P, v, i, j, q, 0.0f, 1.0f);
-      continue;
-    }
-    if (q == 0) {
-      WsRay wr;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        wr.o[a] = ray.o[a];
-        wr.d[a] = ray.d[a];
-      }
-      wr.t_near = ray.t_near;
-      wr.delta = hit ? sample_delta(ray, P.N) : 0.0f;
-      sh->ray[slot][s] = wr;
-    }
-    const uint32_t bh = __ballot_sync(0xffffffffu, hit), bp = __ballot_sync(0xffffffffu, pix);
-    if ((tid & 31) == 0) {
-      reinterpret_cast<uint8_t *>(&sh->slot_hit[slot])[tid >> 5] = (uint8_t)ray_nibble(bh);
-      reinterpret_cast<uint8_t *>(&sh->slot_pix[slot])[tid >> 5] = (uint8_t)ray_nibble(bp);
-    }
-    if (tid == 0) {
-      sh->slot_v[slot] = v;
-      sh->slot_i0[slot] = prow * kPatch;
-      sh->slot_j0[slot] = pcol * kPatch;
-    }
-    ptx::bar_sync(bar_id, 128);
-    return true;
-  }
-}
-
-__global__ void __launch_bounds__(kWsThreads, 1) render_ws_kernel(const __grid_constant__ RenderParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                              ~uintptr_t(1023));
-  uint8_t *tileA0 = smem;
-  uint8_t *tileB0 = smem + kWsGroups * kATileBytes;
-  uint8_t *wsm = tileB0 + kWsGroups * kBTileBytes;
-  const int L = P.L;
-  WsShared *sh = reinterpret_cast<WsShared *>(wsm + (L - 2) * kWHidden + kWHead);
-  const int tid_cta = threadIdx.x;
-  const int warp = tid_cta >> 5;
-
-  // ---- prologue: barriers, TMEM, weights (as render_tc_kernel)
-  if (tid_cta == 0) {
-    for (int i = 0; i < kWsGroups; ++i) {
-      ptx::mbar_init(&sh->full[i], 1);
-      ptx::mbar_init(&sh->empty[i], 1);
-      ptx::mbar_init(&sh->mbar[i], 1);
-      sh->composited[i] = 0u;
-      sh->n_tiles[i] = sh->n_kcols[i] = 0u;
-    }
-    for (int i = 0; i < kWsSlots; ++i) sh->slot_alive[i] = 0u;
-    for (int k = 0; k < kWsSamplers; ++k)
-      for (int p = 0; p < 2; ++p)
-        for (int e = 0; e < 8; ++e) sh->bbox[k][p][e] = (e < 4) ? 0x7fffffff : -1;
-    ptx::fence_mbar_init();
-  }
-  if (warp == 0) ptx::tmem_alloc(&sh->tmem_base, 512);
-  for (int l = 1; l < L; ++l) {
-    const int nout = (l == L - 1) ? 16 : kTcHD;
-    const int nreal = (l == L - 1) ? 4 : kTcHD;
-    uint8_t *wl = wsm + (l - 1) * kWHidden;
-    const __nv_bfloat16 *W = reinterpret_cast<const __nv_bfloat16 *>(P.w[l]);
-    for (int e = tid_cta; e < nout * (int)kWK; e += kWsThreads) {
-      const int n = e / kWK, k = e - n * kWK;
-      float v = 0.0f;
-      if (n < nreal) {
-        if (k < kTcHD) v = __bfloat162float(W[n * kTcHD + k]);
-        else if (k == kTcHD) v = __ldg(P.b[l] + n);
-      }
-      const uint32_t off = (n >> 3) * kWSbo + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
-      *reinterpret_cast<__half *>(wl + off) = __float2half_rn(v);
-    }
-  }
-  if (tid_cta < 4) sh->head_bias[tid_cta] = __ldg(P.b[L - 1] + tid_cta);
-  ptx::fence_proxy_async_smem();
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-
-  const int R = P.R;
-  const int64_t HW = (int64_t)P.H * P.W;
-  unsigned n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;
-
-  if (warp < 4 * kWsGroups) {
-    // =========================================================== MLP group
-    const int g = warp >> 2;
-    const int tid = tid_cta & 127;
-    const int s = tid >> 3, q = tid & 7;
-    const int bar_id = 1 + g;
-    const uint32_t tmem = sh->tmem_base + (uint32_t)(g * 2 * kTcHD);
-    const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
-    const uint32_t sB = ptx::smem_u32(tileB0 + g * kBTileBytes);
-    const uint32_t sW = ptx::smem_u32(wsm);
-    constexpr uint32_t idesc_blend = ptx::idesc_f16(128, kTcHD, 1);
-    constexpr uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
-    constexpr uint32_t idesc_head = ptx::idesc_f16(128, 16, 0);
-    uint32_t fphase = 0, mphase = 0;
-    PH_DECL
-    int cur = 0;  // slot whose ray state is in (T, acc, alive); the other one is parked
-    float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
-    bool alive = false;
-    float To = 1.0f, ao0 = 0.0f, ao1 = 0.0f, ao2 = 0.0f;
-    bool aliveo = false;
-    for (uint32_t n = 0;; ++n) {
-      WS_WAIT(&sh->full[g], fphase);
-      fphase ^= 1u;
-      const int x = sh->desc[g][0], k0 = sh->desc[g][1];
-      int kpad = sh->desc[g][2], flags = sh->desc[g][3];
-      if (flags & kWsDone) break;
-      PH(0);
-      if (x != cur) {
-        float t;
-        t = T; T = To; To = t;
-        t = acc0; acc0 = ao0; ao0 = t;
-        t = acc1; acc1 = ao1; ao1 = t;
-        t = acc2; acc2 = ao2; ao2 = t;
-        const bool b = alive; alive = aliveo; aliveo = b;
-        cur = x;
-      }
-      const int slot = 2 * g + x;
-      if (flags & kWsFirst) {
-        T = 1.0f;
-        acc0 = acc1 = acc2 = 0.0f;
-        alive = ray_bit(sh->slot_hit[slot], s);
-      }
-      // ---- blend (a3) on the tensor cores, one MMA chain per staged window
-      for (;;) {
-        ptx::bar_sync(bar_id, 128);  // everyone has read the descriptor
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          for (int ks = 0; ks < kpad / 16; ++ks) {
-            const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
-            const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-            ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, ((flags & kWsWin0) && ks == 0) ? 0u : 1u);
-          }
-          ptx::mma_commit(&sh->empty[g]);
-          if (flags & kWsLast) ptx::mma_commit(&sh->mbar[g]);
-          sh->n_tiles[g] += 1u;
-          sh->n_kcols[g] += (unsigned)kpad;
-        }
-        if (flags & kWsLast) break;
-        WS_WAIT(&sh->full[g], fphase);
-        fphase ^= 1u;
-        kpad = sh->desc[g][2];
-        flags = sh->desc[g][3];
-      }
-      WS_WAIT(&sh->mbar[g], mphase);
-      mphase ^= 1u;
-      ptx::tc_fence_after();
-      PH(1);
-      const bool sv = alive && (k0 + q < P.N);
-      // ---- MLP layers 1..L-1 (a4)
-      for (int l = 1; l < L; ++l) {
-        act_epilogue(tmem_row, tmem_row + kTcHD);
-        ptx::tc_fence_before();
-        ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
-          ptx::tc_fence_after();
-          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
-          const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
-          const int nks = (l == L - 1) ? kTcHD / 16 : (int)kWK / 16;
-#pragma unroll
-          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            if (ks < nks) {
-              const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-              ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
-            }
-          }
-          ptx::mma_commit(&sh->mbar[g]);
-        }
-        WS_WAIT(&sh->mbar[g], mphase);
-        mphase ^= 1u;
-        ptx::tc_fence_after();
-      }
-      PH(2);
-      uint32_t o4[4];
-      ptx::tmem_ld4(tmem_row, o4);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-      if (sv) {
-        const float *bh = sh->head_bias;
-        const float xx = __uint_as_float(o4[0]) + bh[0] + P.dshift;
-        sigma = __logf(1.0f + __expf(-fabsf(xx))) + fmaxf(xx, 0.0f);
-        const float sc = 1.0f + 2.0f * P.weps;
-        c0 = __fdividef(sc, 1.0f + __expf(-(__uint_as_float(o4[1]) + bh[1]))) - P.weps;
-        c1 = __fdividef(sc, 1.0f + __expf(-(__uint_as_float(o4[2]) + bh[2]))) - P.weps;
-        c2 = __fdividef(sc, 1.0f + __expf(-(__uint_as_float(o4[3]) + bh[3]))) - P.weps;
-        n_samples++;
-      }
-      // ---- a5: composite the ray's 8 samples (8-lane segmented scan)
-      const float delta = sh->ray[slot][s].delta;
-      const float tau = sv ? sigma * delta : 0.0f;
-      float S = tau;
-#pragma unroll
-      for (int sh_ = 1; sh_ < kChunk; sh_ <<= 1) {
-        const float y = __shfl_up_sync(0xffffffffu, S, sh_, kChunk);
-        if (q >= sh_) S += y;
-      }
-      const float Tk = T * __expf(-(S - tau));
-      const float w = Tk * (1.0f - __expf(-tau));
-      acc0 += w * c0;
-      acc1 += w * c1;
-      acc2 += w * c2;
-      const float Stot = __shfl_sync(0xffffffffu, S, kChunk - 1, kChunk);
-      T = T * __expf(-Stot);
-      const bool nxt = k0 + kChunk < P.N;
-      if (alive && P.term_eps > 0.0f && T < P.term_eps) {
-        if (nxt && q == 0) n_term++;
-        alive = false;
-      }
-      const bool cont = alive && nxt;
-      const uint32_t bal = __ballot_sync(0xffffffffu, cont);
-      if ((tid & 31) == 0)
-        reinterpret_cast<volatile uint8_t *>(&sh->slot_alive[slot])[warp & 3] = (uint8_t)ray_nibble(bal);
-      const bool any = ptx::bar_red_or(bar_id, 128, cont);
-      if (!any) {  // ---- the patch is done: reduce the 8 lanes, write rgb/alpha (+ DDIM)
-#pragma unroll
-        for (int sh_ = kChunk / 2; sh_ > 0; sh_ >>= 1) {
-          acc0 += __shfl_xor_sync(0xffffffffu, acc0, sh_, kChunk);
-          acc1 += __shfl_xor_sync(0xffffffffu, acc1, sh_, kChunk);
-          acc2 += __shfl_xor_sync(0xffffffffu, acc2, sh_, kChunk);
-        }
-        if (q < 3 && ray_bit(sh->slot_pix[slot], s)) {
-          const int v = sh->slot_v[slot];
-          const int i = sh->slot_i0[slot] + (s >> 2), j = sh->slot_j0[slot] + (s & 3);
-          ws_ray_out(P, v, i, j, q, q == 0 ? acc0 : (q == 1 ? acc1 : acc2), T);
-        }
-        ptx::bar_sync(bar_id, 128);  // slot data read before the sampler may refill it
-      }
-      if (tid == 0) ptx::sts_release(&sh->composited[g], n + 1);
-      PH(3);
-    }
-#ifdef DMV3D_PHASES
-    if (P.counters && tid == 0)
-      for (int e = 0; e < 4; ++e) atomicAdd(P.counters + 8 + e, ph_acc[e]);
-#endif
-    if (P.counters && tid == 0) {
-      atomicAdd(P.counters + 4, 128ull * sh->n_tiles[g]);
-      atomicAdd(P.counters + 5, (unsigned long long)sh->n_kcols[g]);
-    }
-  } else {
-    // =========================================================== samplers
-    const int k = (warp - 4 * kWsGroups) >> 2;
-    const int tid = tid_cta - 128 * (kWsGroups + k);
-    const int s = tid >> 3, q = tid & 7;
-    const int bar_id = 1 + kWsGroups + k;
-    const __half *G0 = reinterpret_cast<const __half *>(reinterpret_cast<const uint8_t *>(P.tp) + kWsHeader);
-    const int64_t g_stride = ((int64_t)3 * R * R + 1) * kTcHD;
-    unsigned int *counter = reinterpret_cast<unsigned int *>(const_cast<void *>(P.tp));
-    const int v_lo = (int)(P.ray_begin / HW);
-    const int v_hi = (int)((P.ray_end - 1) / HW);
-    const int PH = (P.H + kPatch - 1) / kPatch, PW = (P.W + kPatch - 1) / kPatch;
-    const int TP = P.tile_size / kPatch;
-    int64_t tile_first = 0, tile_n = 0;
-    if (TP > 0) owned_tiles(v_lo, v_hi, P.H, P.W, P.tile_size, P.tile_rank, P.tile_count, tile_first, tile_n);
-    const int64_t TH = TP > 0 ? (P.H + P.tile_size - 1) / P.tile_size : 1;
-    const int64_t TW = TP > 0 ? (P.W + P.tile_size - 1) / P.tile_size : 1;
-    const int64_t npatch = TP > 0 ? tile_n * TP * TP : (int64_t)(v_hi - v_lo + 1) * PH * PW;
-    const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
-    const int hb = P.smode != 0 ? 1 : 0;
-    const WsQueue Q{HW, npatch, tile_first, TH, TW, v_lo, PH, PW, TP, counter};
-    int par = 0;
-    PH_DECL
-
-    // Fetch the next renderable patch into `slot` (all 128 threads): rays, Plucker map,
-    // view skipping, fully-missed patches written out directly.  False: queue exhausted.
-    // Stage chunk k0 of slot x of group f.g: geometry, texel window(s), B rows by cp.async,
-    // sparse A rows; one full arrival per window.
-    auto stage_tile = [&](WsFeed &f, int x, bool first) {
-      PH(1);
-      const int g = f.g;
-      const int slot = 2 * g + x;
-      const int k0 = x ? f.k01 : f.k00;
-      const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
-      const uint32_t sB = ptx::smem_u32(tileB0 + g * kBTileBytes);
-      const uint32_t sArow = sA + a_row(tid);
-      const WsRay rr = sh->ray[slot][s];
-      const int v = sh->slot_v[slot];
-      const __half *G = G0 + (int64_t)(v / P.V_asset) * g_stride;
-      const uint32_t am = first ? sh->slot_hit[slot] : sh->slot_alive[slot];
-      const int kq = k0 + q;
-      const bool sv = ray_bit(am, s) && kq < P.N;
-      int ix[3] = {0, 0, 0};
-      float wl[3] = {0.f, 0.f, 0.f}, wh[3] = {0.f, 0.f, 0.f};
-      if (sv) {
-        Ray ray;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          ray.o[a] = rr.o[a];
-          ray.d[a] = rr.d[a];
-        }
-        ray.t_near = rr.t_near;
-        float u = 0.5f;
-        if (P.jitter) {
-          const int64_t r = (int64_t)v * HW + (int64_t)(sh->slot_i0[slot] + (s >> 2)) * P.W +
-                            sh->slot_j0[slot] + (s & 3);
-          u = jitter_u(P.seed, (uint64_t)r * P.N + kq);
-        }
-        float p[3];
-        sample_p(ray, sample_t(ray, rr.delta, kq, u), p);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
-      }
-      int mn[3], mx[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        mn[a] = __reduce_min_sync(0xffffffffu, sv ? ix[a] : 0x7fffffff);
-        mx[a] = __reduce_max_sync(0xffffffffu, sv ? ix[a] : -1);
-      }
-      if ((tid & 31) == 0) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          atomicMin(&sh->bbox[k][par][a], mn[a]);
-          atomicMax(&sh->bbox[k][par][4 + a], mx[a]);
-        }
-      }
-      ptx::bar_sync(bar_id, 128);
-      const int *bb = sh->bbox[k][par];
-      const int lo0 = bb[0], lo1 = bb[1], lo2 = bb[2];
-      const int ext0 = bb[4] - lo0 + 2, ext1 = bb[5] - lo1 + 2, ext2 = bb[6] - lo2 + 2;
-      if (tid < 8) sh->bbox[k][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
-      par ^= 1;
-      PH(2);
-      const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
-      const int ktex = base2 + ext1 * ext2;
-      const int ktot = ktex + hb;
-      const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
-      const int cols[3] = {cb * ext0 + ca, base1 + cc * ext0 + ca, base2 + cc * ext1 + cb};
-      const int bws[3] = {ext0, ext0, ext1};
-      const float la[3] = {wl[0], wl[0], wl[1]}, ha[3] = {wh[0], wh[0], wh[1]};
-      const float lb[3] = {wl[1], wl[2], wl[2]}, hb3[3] = {wh[1], wh[2], wh[2]};
-      for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
-        if (w0 > 0) WS_WAIT(&sh->empty[g], (f.nwin - 1) & 1u);  // previous window read
-        const int kp = min(kTcKMax, ktot - w0);
-        const int kpad = (kp + 15) & ~15;
-        // B: this thread stages texel row `tid` of the window (SWIZZLE_128B, 8 x 16 B)
-        if (tid < kpad) {
-          const int kg = w0 + tid;
-          int texel = -1;
-          if (kg == ktex && hb) {
-            texel = 3 * R * R;
-          } else if (kg < ktex) {
-            int loc, bw, ta0, tb0, pl;
-            if (kg >= base2) { pl = 2; loc = kg - base2; bw = ext1; ta0 = lo1; tb0 = lo2; }
-            else if (kg >= base1) { pl = 1; loc = kg - base1; bw = ext0; ta0 = lo0; tb0 = lo2; }
-            else { pl = 0; loc = kg; bw = ext0; ta0 = lo0; tb0 = lo1; }
-            const int rr2 = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
-            texel = (pl * R + tb0 + rr2) * R + ta0 + (loc - rr2 * bw);
-          }
-          const uint32_t drow = sB + (uint32_t)(tid << 7);
-          const __half *src = G + (size_t)max(texel, 0) * kTcHD;
-          const uint32_t nb = texel >= 0 ? 16u : 0u;
-#pragma unroll
-          for (int ch = 0; ch < 8; ++ch) ptx::cp_async16(drow + (uint32_t)((ch ^ (tid & 7)) << 4), src + ch * 8, nb);
-        }
-        PH(3);
-        // A: this row's 12 bilinear weights (x 1/3 for the mean) in a zeroed sparse row
-        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
-        if (sv) {
-#pragma unroll
-          for (int pl = 0; pl < 3; ++pl) {
-            const float gy = lb[pl] * wscale, fy = hb3[pl] * wscale;
-            const int c0 = cols[pl] - w0, c2 = c0 + bws[pl];
-            const float w4[4] = {la[pl] * gy, ha[pl] * gy, la[pl] * fy, ha[pl] * fy};
-            const int cs[4] = {c0, c0 + 1, c2, c2 + 1};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if ((unsigned)cs[e] < (unsigned)kp) ptx::sts16(sArow + a_col(cs[e]), ptx::f32_to_f16(w4[e]));
-          }
-          if (hb && (unsigned)(ktex - w0) < (unsigned)kp) ptx::sts16(sArow + a_col(ktex - w0), (uint16_t)0x3c00u);
-        }
-        PH(4);
-        ptx::cp_async_wait_all();
-        ptx::fence_proxy_async_smem();
-        if (tid == 0) {
-          sh->desc[g][0] = x;
-          sh->desc[g][1] = k0;
-          sh->desc[g][2] = kpad;
-          sh->desc[g][3] = (first && w0 == 0 ? kWsFirst : 0) | (w0 == 0 ? kWsWin0 : 0) |
-                           (w0 + kTcKMax >= ktot ? kWsLast : 0);
-        }
-        ptx::bar_sync(bar_id, 128);
-        if (tid == 0) ptx::mbar_arrive(&sh->full[g]);
-        ++f.nwin;
-        PH(5);
-      }
-      if (x) { f.ti1 = f.ntile; f.k01 = k0 + kChunk; }
-      else { f.ti0 = f.ntile; f.k00 = k0 + kChunk; }
-      ++f.ntile;
-      f.last = x;
-    };
-
-    // One tile (or the end marker) for group f.g.
-    auto feed = [&](WsFeed &f) {
-      if (f.done) return;
-      PH(6);
-      if (f.nwin > 0) WS_WAIT(&sh->empty[f.g], (f.nwin - 1) & 1u);  // the stage is free
-      PH(0);
-      int x = f.last ^ 1;
-      for (int attempt = 0; attempt < 2; ++attempt, x ^= 1) {
-        const int st = x ? f.st1 : f.st0;
-        if (st == 2) continue;
-        const int ti = x ? f.ti1 : f.ti0;
-        if (ti >= 0)  // the slot's previous tile is composited: its alive mask is current
-          for (uint32_t spin = 0; (int)ptx::lds_acquire(&sh->composited[f.g]) <= ti; ++spin)
-            WS_SPIN_CHECK(spin);
-        const int slot = 2 * f.g + x;
-        if (st == 1 && sh->slot_alive[slot] != 0u) {
-          stage_tile(f, x, false);
-          return;
-        }
-        PH(0);
-        if (ws_fetch_patch(P, sh, Q, k, tid, slot, n_rays, n_hit)) {
-          if (x) { f.st1 = 1; f.k01 = 0; }
-          else { f.st0 = 1; f.k00 = 0; }
-          stage_tile(f, x, true);
-          return;
-        }
-        if (x) f.st1 = 2;
-        else f.st0 = 2;
-      }
-      if (tid == 0) {  // both slots dead: the group may leave
-        sh->desc[f.g][3] = kWsDone;
-        ptx::mbar_arrive(&sh->full[f.g]);
-      }
-      ++f.nwin;
-      f.done = true;
-    };
-
-    // one copy of the feed code for both groups (the kernel is instruction-cache bound
-    // when it is inlined twice): the two feeds' bookkeeping lives in a local array
-    WsFeed F[2] = {{2 * k, 0u, 0, 1, 0, 0, 0, 0, -1, -1, false},
-                   {2 * k + 1, 0u, 0, 1, 0, 0, 0, 0, -1, -1, false}};
-    for (int jj = 0; !(F[0].done && F[1].done); jj ^= 1) feed(F[jj]);
-    ptx::cp_async_wait_all();
-#ifdef DMV3D_PHASES
-    if (P.counters && tid == 0)
-      for (int e = 0; e < 8; ++e) atomicAdd(P.counters + 16 + e, ph_acc[e]);
-#endif
-  }
-
-  if (P.counters) {
-#pragma unroll
-    for (int s_ = 16; s_ > 0; s_ >>= 1) {
-      n_hit += __shfl_xor_sync(0xffffffffu, n_hit, s_);
-      n_samples += __shfl_xor_sync(0xffffffffu, n_samples, s_);
-      n_term += __shfl_xor_sync(0xffffffffu, n_term, s_);
-      n_rays += __shfl_xor_sync(0xffffffffu, n_rays, s_);
-    }
-    if ((tid_cta & 31) == 0) {
-      atomicAdd(P.counters + 0, (unsigned long long)n_hit);
-      atomicAdd(P.counters + 1, (unsigned long long)n_samples);
-      atomicAdd(P.counters + 2, (unsigned long long)n_term);
-      atomicAdd(P.counters + 3, (unsigned long long)n_rays);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(sh->tmem_base, 512);
-  }
-}
-
 // ------------------------------------------------------------------ launch
 template <int NG, bool GRID>
 static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
@@ -1352,17 +747,6 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   return cudaSuccess;
 }
 
-// The warp-specialised kernel renders when its four stages fit in shared memory;
-// DMV3D_TC_KERNEL=classic forces render_tc_kernel (A/B experiments).
-static bool use_ws(int L) {
-  static const int force = [] {
-    const char *e = getenv("DMV3D_TC_KERNEL");
-    return e ? (strcmp(e, "classic") == 0 ? 0 : 1) : -1;
-  }();
-  if (force == 0) return false;
-  return ws_smem_bytes(L) <= kSmemLimit;
-}
-
 // P.grid_res > 0 selects the density-grid mode (row f3)
 cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   const bool grid_mode = P0.grid_res > 0;
@@ -1398,19 +782,7 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
         return cudaSuccess;
       }
     }
-    if (use_ws(P.L)) {
-      const size_t s1 = ws_smem_bytes(P.L);
-      e = cudaFuncSetAttribute(render_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-      if (e == cudaSuccess) {
-        // every CTA holds up to 8 patches in flight
-        int grid = sms;
-        if ((int64_t)grid * kWsSlots > npatch) grid = (int)std::max<int64_t>(1, (npatch + kWsSlots - 1) / kWsSlots);
-        render_ws_kernel<<<grid, kWsThreads, s1, st>>>(P);
-        e = cudaGetLastError();
-      }
-    } else {
-      e = ng4 ? launch_k1<4, false>(P, sms, npatch, st) : launch_k1<2, false>(P, sms, npatch, st);
-    }
+    e = ng4 ? launch_k1<4, false>(P, sms, npatch, st) : launch_k1<2, false>(P, sms, npatch, st);
   }
   timer_end(P.timer, st);
   return e;
