@@ -73,8 +73,12 @@ typedef enum {
   DMV3D_ENGINE_AUTO = 0,   /* tensor cores when the shapes allow, else SIMT            */
   DMV3D_ENGINE_SIMT = 1,   /* fp32 CUDA-core MLP (fp32 or bf16 storage)                */
   DMV3D_ENGINE_TCGEN05 = 2 /* tensor cores: bf16 storage, blend + MLP as fp16 tcgen05
-                              MMAs with fp32 TMEM accumulation; ReLU, hidden 64, needs
-                              opts.workspace; |values| must stay below 65504 (fp16)     */
+                              MMAs with fp32 TMEM accumulation; hidden 64 (ReLU, SiLU or
+                              softplus hidden layers; the backward: ReLU), needs
+                              opts.workspace.  Projected triplane and activations are
+                              fp16: a value beyond +-65504 is NOT clamped, it becomes
+                              inf / NaN in the outputs and raises the call's range flag
+                              (dmv3d_range_flags)                                       */
 } dmv3d_engine;
 
 /* Camera set C ("viewpoints C = {c_1..c_N}"). */
@@ -127,7 +131,9 @@ typedef struct {
                               TCGEN05 only: [4] tensor-core tile rows issued (128 per
                               blend window: evaluated / issued = MMA row occupancy),
                               [5] staged texel columns (K) summed over blend windows,
-                              [6..7] reserved (0)                                      */
+                              [6] evaluated samples whose head output was not finite
+                              (fp16 overflow upstream, see dmv3d_range_flags),
+                              [7] reserved (0)                                         */
   void *workspace;         /* DEVICE scratch of >= dmv3d_workspace_bytes() bytes, 256-B
                               aligned; required by the TCGEN05 engine (holds the
                               per-step projected triplane), ignored by SIMT.  One
@@ -182,6 +188,28 @@ dmv3d_status dmv3d_timer_read(dmv3d_timer *timer, double *total_ms, int64_t *lau
  * it, the backward's projected-space gradient dG [(3*R*R + 1)][hidden] fp32.
  * Rendering alone needs only 256 + (3*R*R + 1)*hidden*2 bytes. */
 uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp);
+
+/* fp16 range guard of the TCGEN05 engine (the projected triplane G = F W0^T + b0 and the
+ * hidden activations are fp16 MMA operands).  Reads the range flags of the last
+ * TCGEN05 call that used `workspace` (enqueued on `stream`; this call synchronises the
+ * stream): bit 0 = some G value was outside +-65504 (or NaN), bit 1 = some evaluated
+ * sample's head output was not finite (an activation overflowed fp16).  Either bit
+ * means the call's outputs contain inf / NaN: rescale the triplane / weights or use
+ * the SIMT engine (fp32).  0 = in range.  The flags are cleared by every call that
+ * projects the triplane (each TCGEN05 render / DDIM / backward / grid call). */
+#define DMV3D_RANGE_G_OVERFLOW 1u
+#define DMV3D_RANGE_ACT_OVERFLOW 2u
+dmv3d_status dmv3d_range_flags(const void *workspace, uint32_t *flags, dmv3d_stream stream);
+
+/* The engine a render / DDIM call with these arguments runs (AUTO resolved): writes
+ * DMV3D_ENGINE_SIMT or DMV3D_ENGINE_TCGEN05 to *engine, or returns the status the call
+ * would fail with.  AUTO takes the tensor cores whenever they can run the call (bf16
+ * triplane + weights, hidden 64, a workspace) and otherwise the fp32 SIMT engine, which
+ * is ~20x slower at cfg3: callers that need the fast path check it here.  No device
+ * work. */
+dmv3d_status dmv3d_select_engine(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                 const dmv3d_render_opts *opts, int32_t num_assets,
+                                 dmv3d_engine *engine);
 
 /* DDIM x0 -> x_{t-1} (readings A15-A20). */
 typedef struct {
@@ -301,13 +329,16 @@ dmv3d_status dmv3d_density_grid(const dmv3d_triplane *triplane, const dmv3d_mlp 
  * intrinsics, c2w, x_t, z, x_prev, rgb, alpha) a HOST pointer (pinned for
  * async copies).  The workspace owns grow-only device buffers, a copy stream and
  * events; one workspace per thread/stream.  Copies in on `stream`, then the views
- * are rendered in up to 4 view chunks (ray ranges; bitwise the same result as one
+ * are rendered in up to 2 view chunks (ray ranges; bitwise the same result as one
  * launch) and each chunk's outputs are copied out on the workspace's copy stream
  * while the next chunk renders; `stream` waits for the last copy, so the host
  * buffers are valid after `stream` is synchronised. */
 typedef struct dmv3d_workspace dmv3d_workspace;
 dmv3d_status dmv3d_workspace_create(dmv3d_workspace **ws);
 dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws);
+/* Range flags (see dmv3d_range_flags) of the last host-buffer step run with `ws`;
+ * synchronises the workspace's device. */
+dmv3d_status dmv3d_workspace_range_flags(dmv3d_workspace *ws, uint32_t *flags);
 dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_triplane *triplane,
                                          const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
                                          const dmv3d_render_opts *opts,

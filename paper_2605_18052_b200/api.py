@@ -217,6 +217,42 @@ def workspace_for(triplane_s, mlp_s, device, stream=None, assets=1):
     return buf
 
 
+RANGE_G_OVERFLOW, RANGE_ACT_OVERFLOW = 1, 2
+
+
+def dmv3d_range_flags(workspace=None, device=None):
+    """fp16 range flags of the last tensor-core call that used `workspace` (default: this
+    module's cached workspace of `device` / the current stream): bit 0 = the projected
+    triplane left +-65504, bit 1 = an fp16 activation overflowed (non-finite head
+    output).  Non-zero: that call's outputs hold inf / NaN.  Synchronises the stream."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if workspace is None:
+        workspace = _WS_CACHE.get((dev.index, torch.cuda.current_stream(dev).cuda_stream))
+        if workspace is None:
+            return 0
+    out = ct.c_uint32()
+    _abi.check(_abi.lib().dmv3d_range_flags(ct.c_void_p(workspace.data_ptr()), ct.byref(out),
+                                            _stream(dev)))
+    return int(out.value)
+
+
+def dmv3d_select_engine(triplane, mlp: "DeviceMLP", assets=1, aabb_min=(-1.0,) * 3,
+                        aabb_max=(1.0,) * 3, **opts):
+    """The engine a render / DDIM call with these arguments runs: "tcgen05" or "simt"."""
+    dev = triplane.device
+    keep = []
+    tt = triplane_struct(triplane, aabb_min, aabb_max, opts.pop("sample_mode", "align_corners"),
+                         fp8_scale=opts.pop("fp8_scale", 1.0))
+    m = mlp.struct(keep)
+    if "workspace" not in opts:
+        opts["workspace"] = workspace_for(tt, m, dev, torch.cuda.current_stream(dev), assets=assets)
+    o = opts_struct(**opts)
+    e = ct.c_int32()
+    _abi.check(_abi.lib().dmv3d_select_engine(ct.byref(tt), ct.byref(m), ct.byref(o), int(assets),
+                                              ct.byref(e)))
+    return {1: "simt", 2: "tcgen05"}[e.value]
+
+
 def ddim_struct(alpha_bar: np.ndarray, t: int, t_prev: int, eta: float, keep_mask, ddim_views,
                 keep, x0_scale=2.0, x0_shift=-1.0, noise_seed=None, skip_kept_views=False):
     ab = np.ascontiguousarray(alpha_bar, dtype=np.float64)
@@ -370,6 +406,12 @@ class Workspace:
     def __init__(self):
         self.handle = ct.c_void_p()
         _abi.check(_abi.lib().dmv3d_workspace_create(ct.byref(self.handle)))
+
+    def range_flags(self):
+        """fp16 range flags of the last host-buffer step (see dmv3d_range_flags)."""
+        out = ct.c_uint32()
+        _abi.check(_abi.lib().dmv3d_workspace_range_flags(self.handle, ct.byref(out)))
+        return int(out.value)
 
     def close(self):
         if self.handle:

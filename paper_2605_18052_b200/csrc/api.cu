@@ -244,13 +244,13 @@ enum class Engine { SIMT, TC };
 dmv3d_status pick_engine(const dmv3d_triplane *t, const dmv3d_mlp *m, const dmv3d_render_opts *o,
                          Engine &e, int assets = 1) {
   const bool bf16 = (t->dtype == DMV3D_BF16 || t->dtype == DMV3D_FP8_E4M3) && m->dtype == DMV3D_BF16;
-  const bool tc_ok = bf16 && m->hidden_act == DMV3D_ACT_RELU &&
+  const bool tc_ok = bf16 &&
                      tc_supported(t->channels, m->hidden, m->num_layers);
   const bool ws_ok = o->workspace && o->workspace_bytes >= tc_workspace_bytes(t->res, m->hidden, assets);
   if (o->engine == DMV3D_ENGINE_TCGEN05) {
     if (!tc_ok)
       return fail(DMV3D_ERR_UNSUPPORTED,
-                  "engine TCGEN05 needs bf16 triplane + weights, ReLU, hidden 64, channels % 8 == 0 "
+                  "engine TCGEN05 needs bf16 triplane + weights, hidden 64, channels % 8 == 0 "
                   "(<= 256), 2 <= L <= 8");
     if (!ws_ok)
       return fail(DMV3D_ERR_INVALID_ARG,
@@ -735,6 +735,7 @@ struct dmv3d_workspace {
   cudaStream_t copy = nullptr;
   cudaEvent_t ev[kChunks + 1] = {};
   int dev = -1;
+  const void *tc_ws = nullptr;  // the TCGEN05 workspace of the last step (range flags)
 };
 
 static cudaError_t ws_reserve(dmv3d_workspace::Buf &b, size_t bytes) {
@@ -773,6 +774,43 @@ dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws) {
   return DMV3D_OK;
 }
 
+dmv3d_status dmv3d_range_flags(const void *workspace, uint32_t *flags, dmv3d_stream stream) {
+  g_err.clear();
+  CHECK_ARG(workspace && flags, "range_flags: NULL argument");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(flags, static_cast<const uint32_t *>(workspace) + 1, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e, "range_flags");
+}
+
+dmv3d_status dmv3d_workspace_range_flags(dmv3d_workspace *ws, uint32_t *flags) {
+  g_err.clear();
+  CHECK_ARG(ws && flags, "workspace_range_flags: NULL argument");
+  *flags = 0;
+  if (!ws->tc_ws) return DMV3D_OK;  // the last step ran on the fp32 SIMT engine
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(flags, static_cast<const uint32_t *>(ws->tc_ws) + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  return cuda_status(e, "workspace_range_flags");
+}
+
+dmv3d_status dmv3d_select_engine(const dmv3d_triplane *triplane, const dmv3d_mlp *mlp,
+                                 const dmv3d_render_opts *opts, int32_t num_assets,
+                                 dmv3d_engine *engine) {
+  g_err.clear();
+  dmv3d_status s;
+  CHECK_ARG(engine != nullptr, "select_engine: engine is NULL");
+  if ((s = check_triplane(triplane)) != DMV3D_OK) return s;
+  CHECK_ARG(opts != nullptr, "opts is NULL");
+  if ((s = check_mlp(mlp, triplane, opts->agg)) != DMV3D_OK) return s;
+  CHECK_ARG(num_assets >= 1, "select_engine: num_assets must be >= 1");
+  Engine e;
+  if ((s = pick_engine(triplane, mlp, opts, e, num_assets)) != DMV3D_OK) return s;
+  *engine = e == Engine::TC ? DMV3D_ENGINE_TCGEN05 : DMV3D_ENGINE_SIMT;
+  return DMV3D_OK;
+}
+
 dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_triplane *triplane,
                                          const dmv3d_cameras *cams, const dmv3d_mlp *mlp,
                                          const dmv3d_render_opts *opts,
@@ -789,6 +827,27 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
   CHECK_ARG(ddim->ddim_views >= 1 && ddim->ddim_views <= cams->num_views, "ddim: need 1 <= ddim_views <= V");
   if (opts->tile_size)  // the full outputs are copied back: a tile shard would return stale pixels
     return fail(DMV3D_ERR_UNSUPPORTED, "host step: interleaved tiles are a device-buffer option");
+  {  // validate everything the copies and the launch depend on BEFORE any work is enqueued
+    dmv3d_status s0;
+    if ((s0 = check_cams(cams)) != DMV3D_OK) return s0;
+    if ((s0 = check_triplane(triplane)) != DMV3D_OK) return s0;
+    const int64_t nr = (int64_t)cams->num_views * cams->height * cams->width;
+    if ((s0 = check_opts(opts, nr)) != DMV3D_OK) return s0;
+    if ((s0 = check_mlp(mlp, triplane, opts->agg)) != DMV3D_OK) return s0;
+    if (ddim->ddim_views > 64) return fail(DMV3D_ERR_UNSUPPORTED, "ddim: at most 64 DDIM views per call");
+    DdimCoef k0;
+    if ((s0 = ddim_coefficients(ddim, ddim->ddim_views, k0)) != DMV3D_OK) return s0;
+    CHECK_ARG(k0.sigma_t == 0.0f || z != nullptr || ddim->noise_in_kernel,
+              "ddim: eta > 0 needs z or noise_in_kernel");
+    dmv3d_render_opts oe = *opts;  // the workspace the step will provide if none is given
+    if (!oe.workspace) {
+      oe.workspace = reinterpret_cast<void *>(uintptr_t(256));
+      oe.workspace_bytes = dmv3d_workspace_bytes(triplane, mlp);
+      if (!oe.workspace_bytes) oe.workspace = nullptr;
+    }
+    Engine en;
+    if ((s0 = pick_engine(triplane, mlp, &oe, en)) != DMV3D_OK) return s0;
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t V = cams->num_views, HW = (size_t)cams->height * cams->width;
   const size_t tp_bytes = (size_t)3 * triplane->res * triplane->res * triplane->channels *
@@ -862,6 +921,7 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
   const size_t vpc = (V + nc - 1) / nc;
   const size_t dv = (size_t)ddim->ddim_views;
   const bool tc = o.workspace != nullptr && o.engine != DMV3D_ENGINE_SIMT;
+  ws->tc_ws = tc ? o.workspace : nullptr;
   for (int k = 0; k < nc; ++k) {
     const size_t v0 = k * vpc, v1 = (v0 + vpc < V) ? v0 + vpc : V;
     if (v0 >= v1) break;

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(256)
     preproject_kernel(const void *__restrict__ Fv, int ntex, int C, int wstride,
                       const __nv_bfloat16 *__restrict__ W0, const float *__restrict__ b0,
                       float bscale, float fscale, __half *__restrict__ G, unsigned int *counter,
-                      __half *__restrict__ gbias, int64_t per_asset, int assets) {
+                      __half *__restrict__ gbias, int64_t per_asset, int assets,
+                      unsigned int *range_flags) {
   extern __shared__ __align__(16) float2 swt[];  // [C][HD/2] (o pairs)
   for (int e = threadIdx.x; e < kTcHD * C; e += blockDim.x) {  // o fastest: conflict-free stores
     const int c = e / kTcHD, o = e - c * kTcHD;
@@ -180,7 +181,10 @@ __global__ void __launch_bounds__(256)
       a1 += b1s;
       cur = nxt;
     }
-    const uint32_t pk = (uint32_t)ptx::f32_to_f16(a0) | ((uint32_t)ptx::f32_to_f16(a1) << 16);
+    // fp16 range guard: G outside +-65504 (or NaN) raises range flag bit 0; the value is
+    // stored as inf / NaN (no silent clamp), so the affected outputs are non-finite
+    if (!(fabsf(a0) <= 65504.0f && fabsf(a1) <= 65504.0f)) atomicOr(range_flags, 1u);
+    const uint32_t pk = ptx::pack_f16x2(a0, a1);
     const int64_t ta = t / per_asset;  // asset: its G block has one extra (bias) row
     reinterpret_cast<uint32_t *>(G + (t + ta) * kTcHD)[lane] = pk;
   }
@@ -195,6 +199,21 @@ __device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(((k >> 3) <
 // epilogue of one MLP layer: accumulator row (HD fp32 TMEM columns at `d_row`) ->
 // ReLU -> fp16 pairs -> the next layer's A operand in TMEM at `a_row` (HD/2 columns),
 // plus the bias column (k = HD: 1.0, k = HD+1..HD+15: 0)
+// hidden activation (reading A5) -> fp16 pair; ReLU folds into the conversion, SiLU and
+// softplus are evaluated in fp32 (fast-math exp / log, within the tensor-core tolerance)
+template <int ACT>
+__device__ __forceinline__ uint32_t pack_act(float lo, float hi) {
+  if constexpr (ACT == 1) {
+    return ptx::pack_f16x2(__fdividef(lo, 1.0f + __expf(-lo)), __fdividef(hi, 1.0f + __expf(-hi)));
+  } else if constexpr (ACT == 2) {
+    return ptx::pack_f16x2(fmaxf(lo, 0.0f) + __logf(1.0f + __expf(-fabsf(lo))),
+                           fmaxf(hi, 0.0f) + __logf(1.0f + __expf(-fabsf(hi))));
+  } else {
+    return ptx::pack_relu_f16x2_inf(lo, hi);
+  }
+}
+
+template <int ACT>
 __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -204,7 +223,7 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
     uint32_t pk[16];
     const float *f = reinterpret_cast<const float *>(v);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_relu_f16x2(f[2 * e], f[2 * e + 1]);
+    for (int e = 0; e < 16; ++e) pk[e] = pack_act<ACT>(f[2 * e], f[2 * e + 1]);
     ptx::tmem_st16(a_row + 16 * h, pk);
   }
   const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -215,7 +234,7 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 // GRID = false: the renderer (rays, compositing, DDIM epilogue).  GRID = true: the
 // density grid (row f3): a "patch" is an 8x4x4 block of grid points, decoded in one
 // 128-row tile through the same staged-texel blend + MLP MMAs.
-template <int NG, bool GRID>
+template <int NG, bool GRID, int ACT>
 __global__ void __launch_bounds__(128 * NG, 1)
     render_tc_kernel(const __grid_constant__ RenderParams P) {
   extern __shared__ uint8_t smem_raw[];
@@ -314,6 +333,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
   uint32_t mphase = 0;
   unsigned n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;  // per thread: fits 32 bits
+  unsigned n_range = 0;  // samples whose head output is not finite (fp16 overflow upstream)
   PH_DECL
   int chunk_ctr = 0;
 
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       // ---- MLP layers 1..L-1 on the tensor cores: fp16 activations live in TMEM
       //      (A operand from TMEM), weights in shared memory
       for (int l = 1; l < L; ++l) {
-        act_epilogue(tmem_row, tmem_row + kTcHD);
+        act_epilogue<ACT>(tmem_row, tmem_row + kTcHD);
         PH(4);
         ptx::tc_fence_before();
         ptx::bar_sync(bar_id, 128);
@@ -594,6 +614,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ptx::tc_fence_before();
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
+        // an inf / NaN anywhere upstream (G or an fp16 activation out of range) reaches the
+        // head: count it (range flag bit 1)
+        const float chk = __uint_as_float(o4[0]) + __uint_as_float(o4[1]) + __uint_as_float(o4[2]) +
+                          __uint_as_float(o4[3]);
+        n_range += (fabsf(chk) < INFINITY) ? 0u : 1u;
         const float *bh = sh->head_bias;  // shared memory: broadcast reads
         const float x = __uint_as_float(o4[0]) + bh[0] + P.dshift;
         sigma = __logf(1.0f + __expf(-fabsf(x))) + fmaxf(x, 0.0f);
@@ -656,9 +681,12 @@ __global__ void __launch_bounds__(128 * NG, 1)
   if (P.counters && tid == 0)
     for (int i = 0; i < 8; ++i) atomicAdd(P.counters + 8 + i, ph_acc[i]);
 #endif
+  if (__any_sync(0xffffffffu, n_range != 0u) && (tid & 31) == 0)
+    atomicOr(reinterpret_cast<unsigned int *>(const_cast<void *>(P.tp)) + 1, 2u);
   if (P.counters) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
+      n_range += __shfl_xor_sync(0xffffffffu, n_range, s);
       n_hit += __shfl_xor_sync(0xffffffffu, n_hit, s);
       n_samples += __shfl_xor_sync(0xffffffffu, n_samples, s);
       n_term += __shfl_xor_sync(0xffffffffu, n_term, s);
@@ -669,6 +697,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       atomicAdd(P.counters + 1, (unsigned long long)n_samples);
       atomicAdd(P.counters + 2, (unsigned long long)n_term);
       atomicAdd(P.counters + 3, (unsigned long long)n_rays);
+      if (n_range) atomicAdd(P.counters + 6, (unsigned long long)n_range);
     }
     if (tid == 0) {  // MMA rows issued (128 per blend window) and staged K columns
       atomicAdd(P.counters + 4, 128ull * sh->n_tiles[g]);
@@ -684,16 +713,22 @@ __global__ void __launch_bounds__(128 * NG, 1)
 }
 
 // ------------------------------------------------------------------ launch
-template <int NG, bool GRID>
-static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
+template <int NG, bool GRID, int ACT>
+static cudaError_t launch_k1a(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
   const size_t s1 = tc_smem_bytes<NG>(P.L);
-  cudaError_t e = cudaFuncSetAttribute(render_tc_kernel<NG, GRID>,
+  cudaError_t e = cudaFuncSetAttribute(render_tc_kernel<NG, GRID, ACT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
   if (e != cudaSuccess) return e;
   int grid = sms;
   if ((int64_t)grid * NG > npatch) grid = (int)((npatch + NG - 1) / NG);
-  render_tc_kernel<NG, GRID><<<grid, 128 * NG, s1, st>>>(P);
+  render_tc_kernel<NG, GRID, ACT><<<grid, 128 * NG, s1, st>>>(P);
   return cudaGetLastError();
+}
+template <int NG, bool GRID>
+static cudaError_t launch_k1(const RenderParams &P, int sms, int64_t npatch, cudaStream_t st) {
+  if (P.act == 1) return launch_k1a<NG, GRID, 1>(P, sms, npatch, st);  // SiLU
+  if (P.act == 2) return launch_k1a<NG, GRID, 2>(P, sms, npatch, st);  // softplus
+  return launch_k1a<NG, GRID, 0>(P, sms, npatch, st);                  // ReLU
 }
 
 // K0 alone (shared with the tensor-core backward): G = F W0^T + b0 * bscale (fp16)
@@ -711,7 +746,11 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   const int A = P.V / P.V_asset;  // assets of a batched launch (each its own G block)
   const size_t s0 = (size_t)kTcHD * P.C * 4;
   auto kern = P.tp_fp8 ? preproject_kernel<true> : preproject_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
+  // range flags (header word 1) of this call: cleared here, raised by K0 (bit 0) and
+  // the render kernel (bit 1)
+  cudaError_t e = cudaMemsetAsync(counter + 1, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0);
   if (e != cudaSuccess) return e;
   const float bscale = P.smode != 0 ? 0.0f : (P.agg == 0 ? 1.0f : (1.0f / 3.0f));
   const uint8_t *F = static_cast<const uint8_t *>(P.tp);
@@ -727,7 +766,7 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
     int64_t g0 = (nt * 32 + 255) / 256;
     if (g0 > sms * DMV3D_K0_BLOCKS_PER_SM) g0 = sms * DMV3D_K0_BLOCKS_PER_SM;
     kern<<<(int)g0, 256, s0, st>>>(F, (int)nt, P.C, P.C, W0, P.b[0], bscale, P.tp_scale, G, counter,
-                                   G + (size_t)ntex * kTcHD, ntex, A);
+                                   G + (size_t)ntex * kTcHD, ntex, A, counter + 1);
     return cudaGetLastError();
   }
   // concat: plane p of every asset is projected by its own column block of W0
@@ -740,7 +779,8 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
       kern<<<g0, 256, s0, st>>>(F + ((size_t)a * 3 + pl) * nt * P.C * esz, nt, P.C, 3 * P.C,
                                 W0 + (size_t)pl * P.C, P.b[0], bscale, P.tp_scale,
                                 G + a * gs + (size_t)pl * nt * kTcHD, first ? counter : nullptr,
-                                first ? G + (size_t)ntex * kTcHD : nullptr, ntex, first ? A : 0);
+                                first ? G + (size_t)ntex * kTcHD : nullptr, ntex, first ? A : 0,
+                                counter + 1);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }

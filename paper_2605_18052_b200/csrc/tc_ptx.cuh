@@ -216,6 +216,14 @@ __device__ __forceinline__ uint32_t pack_relu_f16x2(float lo, float hi) {
   asm("cvt.rn.relu.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// relu(a), relu(b) -> packed f16x2 WITHOUT saturation: a value beyond the fp16 range
+// becomes +inf, so an overflowed activation reaches the head output as inf / NaN,
+// where the renderer detects it (range flag)
+__device__ __forceinline__ uint32_t pack_relu_f16x2_inf(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 // (lo, hi) -> packed f16x2, lo in the low half, round to nearest
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   uint32_t r;
