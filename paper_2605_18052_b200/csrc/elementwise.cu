@@ -164,27 +164,114 @@ __global__ void sample_points_kernel(const __grid_constant__ RenderParams P, flo
   }
 }
 
-// row f2: Plucker ray map [V][6][H][W] for rays [ray_begin, ray_end); one thread
-// per (ray, component) so the 6 planar stores of a warp are coalesced
-__global__ void plucker_kernel(const __grid_constant__ RenderParams P, float *out) {
-  const int64_t n = (P.ray_end - P.ray_begin) * 6;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+// row f2: Plucker ray map [V][6][H][W] for rays [ray_begin, ray_end).
+// One thread per 4 consecutive rays of a view (HBM-bound: 24 B written per ray, nothing
+// read but the cameras): origin and unit direction with make_ray's exact IEEE operation
+// order (bit-identical), no AABB slab test (the map does not need it), and six planar
+// float4 stores per thread -- a warp writes 512 contiguous bytes per component plane.
+__device__ __forceinline__ void pixel_ray(const float *__restrict__ intr, const float *__restrict__ c2w,
+                                          int v, int i, int j, float o[3], float d[3]) {
+  const float *K = intr + 4 * v;
+  const float *M = c2w + 12 * v;
+  const float xc = __fdiv_rn(__fsub_rn(__fadd_rn(__int2float_rn(j), 0.5f), __ldg(K + 2)), __ldg(K + 0));
+  const float yc = __fdiv_rn(__fsub_rn(__fadd_rn(__int2float_rn(i), 0.5f), __ldg(K + 3)), __ldg(K + 1));
+  float dw[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float s = __fadd_rn(__fmul_rn(__ldg(M + 4 * a + 0), xc), __fmul_rn(__ldg(M + 4 * a + 1), yc));
+    dw[a] = __fadd_rn(s, __ldg(M + 4 * a + 2));
+  }
+  const float nn = __fadd_rn(__fadd_rn(__fmul_rn(dw[0], dw[0]), __fmul_rn(dw[1], dw[1])),
+                             __fmul_rn(dw[2], dw[2]));
+  const float n = __fsqrt_rn(nn);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d[a] = __fdiv_rn(dw[a], n);
+    o[a] = __ldg(M + 4 * a + 3);
+  }
+}
+
+__device__ __forceinline__ void plucker6(const float o[3], const float d[3], float m[6]) {
+  Ray r;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.o[a] = o[a];
+    r.d[a] = d[a];
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) m[c] = plucker_component(r, c);
+}
+
+template <int RPT> struct VecT;
+template <> struct VecT<1> { using T = float; };
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<4> { using T = float4; };
+__device__ __forceinline__ float vec_of(const float (&m)[1][6], int c) { return m[0][c]; }
+__device__ __forceinline__ float2 vec_of(const float (&m)[2][6], int c) { return make_float2(m[0][c], m[1][c]); }
+__device__ __forceinline__ float4 vec_of(const float (&m)[4][6], int c) {
+  return make_float4(m[0][c], m[1][c], m[2][c], m[3][c]);
+}
+
+// vector path: RPT consecutive rays per thread, HW % RPT == 0 and ray_begin, ray_end
+// multiples of RPT (every group lies in one view; its outputs are one aligned RPT-wide
+// store per plane).  RPT is chosen per launch: wide stores when there are enough rays to
+// fill the machine, one ray per thread (more rays in flight) otherwise.
+template <int RPT>
+__global__ void __launch_bounds__(256) plucker_vec_kernel(const __grid_constant__ RenderParams P, float *out) {
+  using V = typename VecT<RPT>::T;
+  const int64_t HW = (int64_t)P.H * P.W;
+  const int64_t nv = (P.ray_end - P.ray_begin) / RPT;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nv;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rr = q % (P.ray_end - P.ray_begin);
-    const int c = (int)(q / (P.ray_end - P.ray_begin));
-    int v, i, j;
-    ray_pixel(P.ray_begin + rr, P.H, P.W, v, i, j);
-    const Ray ray = make_ray(P.intr, P.c2w, v, i, j, P.lo, P.hi);
-    plucker_write(out, P.H, P.W, v, i, j, c, ray);
+    const int64_t r0 = P.ray_begin + RPT * q;
+    int v, pix0;
+    if (P.ray_end < (int64_t(1) << 31)) {  // 32-bit index math (every realistic launch)
+      v = (int)r0 / (int)HW;
+      pix0 = (int)r0 - v * (int)HW;
+    } else {
+      v = (int)(r0 / HW);
+      pix0 = (int)(r0 - (int64_t)v * HW);
+    }
+    float m[RPT][6];
+#pragma unroll
+    for (int e = 0; e < RPT; ++e) {
+      const int pix = pix0 + e;
+      const int i = pix / P.W, j = pix - i * P.W;
+      float o[3], d[3];
+      pixel_ray(P.intr, P.c2w, v, i, j, o, d);
+      plucker6(o, d, m[e]);
+    }
+    V *dst = reinterpret_cast<V *>(out + (int64_t)v * 6 * HW + pix0);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) __stcs(dst + c * (HW / RPT), vec_of(m, c));
   }
 }
 
 cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st) {
-  const int64_t n = (P.ray_end - P.ray_begin) * 6;
+  const int64_t n = P.ray_end - P.ray_begin;
   if (n <= 0) return cudaSuccess;
-  const int64_t grid = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t HW = (int64_t)P.H * P.W;
+  auto fits = [&](int r) {
+    return HW % r == 0 && P.ray_begin % r == 0 && P.ray_end % r == 0 &&
+           (reinterpret_cast<uintptr_t>(out) & (4u * r - 1)) == 0;
+  };
+  // rays per thread: float4 stores once every thread of two full waves (2048 threads
+  // per SM) has 4 rays, else float2 / scalar for more rays in flight
+  const int64_t wave2 = (int64_t)sms * 2048 * 2;
+  const int rpt = (fits(4) && n / 4 >= wave2) ? 4 : (fits(2) && n / 2 >= wave2) ? 2 : 1;
+  const int64_t items = n / rpt;
+  int64_t grid = (items + 255) / 256;  // one item per thread (grid-stride only if huge)
+  if (grid > (int64_t)sms * 256) grid = (int64_t)sms * 256;
   timer_begin(P.timer, st);
-  plucker_kernel<<<(int)grid, 256, 0, st>>>(P, out);
+  if (rpt == 4)
+    plucker_vec_kernel<4><<<(int)grid, 256, 0, st>>>(P, out);
+  else if (rpt == 2)
+    plucker_vec_kernel<2><<<(int)grid, 256, 0, st>>>(P, out);
+  else
+    plucker_vec_kernel<1><<<(int)grid, 256, 0, st>>>(P, out);
   timer_end(P.timer, st);
   return cudaGetLastError();
 }

@@ -35,6 +35,46 @@ def test_plucker_standalone_bit_exact():
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("H,W,rng", [(16, 12, None), (16, 12, (4, 1532)), (16, 12, (3, 1001)),
+                                     (9, 7, (10, 400))],
+                         ids=["vec", "vec-range", "scalar-range", "scalar-ragged"])
+def test_plucker_standalone_paths_bit_exact(H, W, rng):
+    """The float4 path (H W % 4 == 0, 4-aligned ray range) and the scalar path, with ray
+    ranges that start and end inside a view: bit-exact against the oracle, pixels outside
+    the range untouched."""
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 4), wl.novel_cameras(H, W, 4, seed=9))
+    intr, c2w = dev_cams(cams)
+    out = torch.full((8, 6, H, W), -7.0, device="cuda")
+    api.dmv3d_plucker_rays(intr, c2w, H, W, out=out, ray_range=rng)
+    g = out.cpu().numpy().transpose(0, 2, 3, 1).reshape(-1, 6)
+    n = 8 * H * W
+    lo, hi = rng if rng else (0, n)
+    want = oracle.plucker(cams, np.arange(lo, hi))
+    assert np.array_equal(g[lo:hi].view(np.uint32), want.view(np.uint32))
+    assert (g[:lo] == -7.0).all() and (g[hi:] == -7.0).all()
+
+
+@pytest.mark.parametrize("V,H,W,rng", [(10, 512, 512, None), (10, 510, 251, None),
+                                       (10, 512, 512, (1024, 2600000))],
+                         ids=["float4", "float2", "float4-range"])
+def test_plucker_standalone_wide_stores_bit_exact(V, H, W, rng):
+    """Launches big enough for 4 / 2 rays per thread (float4 / float2 planar stores):
+    a seeded subset of 20k rays (plus both ends of the range) bit-exact against the
+    oracle, every value in the range written, the rest untouched."""
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 4), wl.novel_cameras(H, W, V - 4, seed=9))
+    intr, c2w = dev_cams(cams)
+    out = torch.full((V, 6, H, W), float("nan"), device="cuda")
+    api.dmv3d_plucker_rays(intr, c2w, H, W, out=out, ray_range=rng)
+    g = out.permute(0, 2, 3, 1).reshape(-1, 6).cpu().numpy()
+    n = V * H * W
+    lo, hi = rng if rng else (0, n)
+    ids = np.unique(np.concatenate([np.random.default_rng(5).integers(lo, hi, 20000), [lo, hi - 1]]))
+    want = oracle.plucker(cams, ids)
+    assert np.array_equal(g[ids].view(np.uint32), want.view(np.uint32))
+    assert np.isfinite(g[lo:hi]).all()
+    assert np.isnan(g[:lo]).all() and np.isnan(g[hi:]).all()
+
+
 @pytest.mark.parametrize("engine,dtype", [("simt", "f32"), ("tcgen05", "bf16")])
 def test_plucker_emitted_by_the_renderer(engine, dtype):
     tp = wl.blob_triplane(16, 32, seed=2)

@@ -48,31 +48,34 @@ def timed(fn, reps, flush):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--rows", default="f1,f2,f3", help="comma list of rows to measure")
     args = ap.parse_args()
     dev = torch.device("cuda")
     flush = torch.empty(64 << 20, device=dev)
     pk = peaks()
     out = []
 
-    # f2: Plucker ray map, 8 views 256^2
-    cams = wl.concat_cameras(wl.input_cameras(256, 256, 4), wl.novel_cameras(256, 256, 4))
-    intr = torch.from_numpy(cams.intrinsics).to(dev)
-    c2w = torch.from_numpy(cams.c2w).to(dev)
-    pl = torch.empty((8, 6, 256, 256), device=dev)
+    # f2: Plucker ray map at 8 views 256^2 and 32 views 512^2 (201 MB written)
+    import ctypes as ct
+    rows = set(args.rows.split(","))
+    for V, S in (((8, 256), (32, 512)) if "f2" in rows else ()):
+        cams = wl.concat_cameras(wl.input_cameras(S, S, 4), wl.novel_cameras(S, S, V - 4))
+        intr = torch.from_numpy(cams.intrinsics).to(dev)
+        c2w = torch.from_numpy(cams.c2w).to(dev)
+        pl = torch.empty((V, 6, S, S), device=dev)
 
-    def f2(timer):
-        c = api.cameras_struct(intr, c2w, 256, 256)
-        o = api.opts_struct(samples_per_ray=1, timer=timer)
-        import ctypes as ct
-        api._abi.check(api._abi.lib().dmv3d_plucker_rays(ct.byref(c), ct.byref(o), pl.data_ptr(),
-                                                         api._stream(dev)))
-    ms = timed(f2, args.reps, flush)
-    rays = 8 * 256 * 256
-    gbs = rays * 24 / (ms / 1e3) / 1e9
-    out.append({"row": "f2 plucker ray map", "metric": "rays/s", "value": rays / (ms / 1e3),
-                "kernel_ms": ms, "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"],
-                                              "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
-                                              "algorithmic": "24 B written per ray"}})
+        def f2(timer):
+            c = api.cameras_struct(intr, c2w, S, S)
+            o = api.opts_struct(samples_per_ray=1, timer=timer)
+            api._abi.check(api._abi.lib().dmv3d_plucker_rays(ct.byref(c), ct.byref(o), pl.data_ptr(),
+                                                             api._stream(dev)))
+        ms = timed(f2, args.reps, flush)
+        rays = V * S * S
+        gbs = rays * 24 / (ms / 1e3) / 1e9
+        out.append({"row": "f2 plucker ray map", "config": f"{V} views {S}^2", "metric": "rays/s",
+                    "value": rays / (ms / 1e3), "kernel_ms": ms,
+                    "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                 "frac": gbs / pk["hbm_gbs"], "algorithmic": "24 B written per ray"}})
 
     # f3: density grid 128^3, C = 80, L = 4 (bf16 storage, fp32 SIMT decode)
     w = wl.make_workload("cfg3")
@@ -80,7 +83,7 @@ def main():
     mlp = api.DeviceMLP.from_host(w.mlp, "bf16", dev)
     G = 128
 
-    for engine in ("simt", "tcgen05"):
+    for engine in (("simt", "tcgen05") if "f3" in rows else ()):
         def f3(timer):
             api.dmv3d_density_grid(tp, mlp, G, timer=timer, engine=engine)
         ms = timed(f3, args.reps, flush)
@@ -100,6 +103,10 @@ def main():
                     "config": f"128^3 grid, C=80, MLP 80-64-64-64-4, bf16 storage, {engine}",
                     "roofline": roof})
 
+    if "f1" not in rows:
+        for line in out:
+            print(json.dumps(line))
+        return
     # f1: renderer backward, 8 views of 128^2 training crops, N = 128
     cams = wl.concat_cameras(wl.input_cameras(128, 128, 4), wl.novel_cameras(128, 128, 4))
     intr = torch.from_numpy(cams.intrinsics).to(dev)
