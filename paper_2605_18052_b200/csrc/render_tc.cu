@@ -61,6 +61,7 @@ constexpr int kTcKMax = 128;    // max staged texels (K) per MMA pass
 constexpr int kPatch = 4;       // 4x4 rays per patch
 constexpr int kChunk = 8;       // samples per ray per tile
 constexpr int kGridKZ = 4;      // density grid: 8x4x4 point blocks per patch column (chunks)
+constexpr uint32_t kHeadAlt = 112;  // second head accumulator: spare TMEM columns of a group
 constexpr uint32_t kWsHeader = kTcWsHeader;
 
 // shared-memory carve-up (bytes)
@@ -196,9 +197,6 @@ __device__ __forceinline__ uint32_t a_row(int m) {
 }
 __device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(((k >> 3) << 7) | ((k & 7) << 1)); }
 
-// epilogue of one MLP layer: accumulator row (HD fp32 TMEM columns at `d_row`) ->
-// ReLU -> fp16 pairs -> the next layer's A operand in TMEM at `a_row` (HD/2 columns),
-// plus the bias column (k = HD: 1.0, k = HD+1..HD+15: 0)
 // hidden activation (reading A5) -> fp16 pair; ReLU folds into the conversion, SiLU and
 // softplus are evaluated in fp32 (fast-math exp / log, within the tensor-core tolerance)
 template <int ACT>
@@ -213,6 +211,10 @@ __device__ __forceinline__ uint32_t pack_act(float lo, float hi) {
   }
 }
 
+// epilogue of one MLP layer: accumulator row (HD fp32 TMEM columns at `d_row`) ->
+// activation -> fp16 pairs -> the next layer's A operand in TMEM at `a_row` (HD/2
+// columns).  The bias K block that follows it (k = HD: 1.0, k = HD+1..HD+15: 0) is
+// constant and written once per kernel.
 template <int ACT>
 __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
 #pragma unroll
@@ -226,8 +228,6 @@ __device__ __forceinline__ void act_epilogue(uint32_t d_row, uint32_t a_row) {
     for (int e = 0; e < 16; ++e) pk[e] = pack_act<ACT>(f[2 * e], f[2 * e + 1]);
     ptx::tmem_st16(a_row + 16 * h, pk);
   }
-  const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-  ptx::tmem_st8(a_row + kTcHD / 2, bias);
   ptx::tmem_st_wait();
 }
 
@@ -290,6 +290,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = sh->tmem_base + (uint32_t)(g * 2 * kTcHD);
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  {  // the activation operand's bias K block ([1, 0 x 15] per row) is constant: once
+    const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    ptx::tmem_st8(tmem_row + kTcHD + kTcHD / 2, bias);
+    ptx::tmem_st_wait();
+  }
 
   const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
   const uint32_t sB = ptx::smem_u32(tileB0 + g * kBTileBytes);
@@ -592,10 +597,20 @@ __global__ void __launch_bounds__(128 * NG, 1)
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
           // the head skips its bias K block (4 FADDs at readout instead of an MMA)
-          const int nks = (l == L - 1) ? kTcHD / 16 : (int)kWK / 16;
+          if (l == L - 1) {
+            // head: K = 64 as two independent 2-step chains (D and the spare columns
+            // [112, 128) of the group's TMEM), summed at readout -- half the dependent steps
 #pragma unroll
-          for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-            if (ks < nks) {
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+              for (int hx = 0; hx < 2; ++hx) {
+                const int kk = 2 * hx + ks;
+                const uint64_t bd = ptx::smem_desc(wbase + kk * 256, 128, kWSbo, 0);
+                ptx::mma_f16_ts(tmem + (hx ? kHeadAlt : 0u), tmem + kTcHD + kk * 8, bd, id, ks > 0 ? 1u : 0u);
+              }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < (int)kWK / 16; ++ks) {
               const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
               ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
             }
@@ -610,7 +625,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
       // ---- head: sigma, rgb (a4)
       uint32_t o4[4];
       ptx::tmem_ld4(tmem_row, o4);
+      uint32_t o4b[4];
+      ptx::tmem_ld4(tmem_row + kHeadAlt, o4b);
       ptx::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o4[e] = __float_as_uint(__uint_as_float(o4[e]) + __uint_as_float(o4b[e]));
       ptx::tc_fence_before();
       float sigma = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
       if (sv) {
