@@ -103,7 +103,7 @@ def main():
                     "config": f"128^3 grid, C=80, MLP 80-64-64-64-4, bf16 storage, {engine}",
                     "roofline": roof})
 
-    if "f1" not in rows:
+    if "f1" not in rows and "f1tc" not in rows:
         for line in out:
             print(json.dumps(line))
         return
@@ -114,21 +114,23 @@ def main():
     g = torch.randn((8, 3, 128, 128), device=dev)
     gA = torch.randn((8, 128, 128), device=dev)
 
-    def f1(timer):
-        api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
-                                  timer=timer)
-    ms = timed(f1, max(3, args.reps // 3), flush)
     rays = 8 * 128 * 128
-    # algorithmic work per sample: two forward MLP+gather passes, dL/dh (MLP^T), dW (outer
-    # products) and the gather transpose
-    per = 2 * (27136 + 1920) + 27136 + 27136 + 1920
-    hitfrac = 0.95
-    fl = rays * hitfrac * 128 * per / (ms / 1e3) / 1e12
-    out.append({"row": "f1 renderer backward", "metric": "rays/s", "value": rays / (ms / 1e3),
-                "kernel_ms": ms, "config": "8 views 128^2, N=128, C=80, L=4, fp32 SIMT, atomics",
-                "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
-                             "frac": fl / FP32_PEAK,
-                             "algorithmic": f"{per} FLOP per sample x ~0.95 hit x 128 samples"}})
+    if "f1" in rows:  # the fp32 SIMT backward (slow: skipped by --rows f1tc)
+        def f1(timer):
+            api.dmv3d_render_backward(tp, intr, c2w, 128, 128, mlp, g, gA, samples_per_ray=128,
+                                      timer=timer)
+        ms = timed(f1, max(3, args.reps // 3), flush)
+        rays = 8 * 128 * 128
+        # algorithmic work per sample: two forward MLP+gather passes, dL/dh (MLP^T), dW (outer
+        # products) and the gather transpose
+        per = 2 * (27136 + 1920) + 27136 + 27136 + 1920
+        hitfrac = 0.95
+        fl = rays * hitfrac * 128 * per / (ms / 1e3) / 1e12
+        out.append({"row": "f1 renderer backward", "metric": "rays/s", "value": rays / (ms / 1e3),
+                    "kernel_ms": ms, "config": "8 views 128^2, N=128, C=80, L=4, fp32 SIMT, atomics",
+                    "roofline": {"bound": "alu", "achieved": fl, "peak": FP32_PEAK, "unit": "TFLOP/s",
+                                 "frac": fl / FP32_PEAK,
+                                 "algorithmic": f"{per} FLOP per sample x ~0.95 hit x 128 samples"}})
 
     # f1 on the tensor cores (engine tcgen05): same workload; whole call (memset, K0
     # projection, the backward kernel, dF / dW0 maps) and the backward kernel alone
