@@ -1,5 +1,7 @@
 // elementwise.cu -- standalone DDIM step (row a6) and the stage-level debug
 // kernels for rows a1-a3 (bit-exact geometry dumps).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -259,9 +261,14 @@ cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st) {
            (reinterpret_cast<uintptr_t>(out) & (4u * r - 1)) == 0;
   };
   // rays per thread: float4 stores once every thread of two full waves (2048 threads
-  // per SM) has 4 rays, else float2 / scalar for more rays in flight
-  const int64_t wave2 = (int64_t)sms * 2048 * 2;
-  const int rpt = (fits(4) && n / 4 >= wave2) ? 4 : (fits(2) && n / 2 >= wave2) ? 2 : 1;
+  // per SM) has 4 rays; float2 down to half a wave (measured at 8 x 256^2: 6.5 us kernel
+  // vs 6.7 / 6.8 for 1 / 4 rays per thread); scalar below
+  const int64_t wave = (int64_t)sms * 2048;
+  int rpt = (fits(4) && n / 4 >= 2 * wave) ? 4 : (fits(2) && n / 2 >= wave / 2) ? 2 : 1;
+  if (const char *f = getenv("DMV3D_PLUCKER_RPT")) {  // A/B override (tools)
+    const int r = atoi(f);
+    if ((r == 1 || r == 2 || r == 4) && fits(r)) rpt = r;
+  }
   const int64_t items = n / rpt;
   int64_t grid = (items + 255) / 256;  // one item per thread (grid-stride only if huge)
   if (grid > (int64_t)sms * 256) grid = (int64_t)sms * 256;
