@@ -203,3 +203,71 @@ def test_render_validation_fuzz():
         assert len(_abi.lib().dmv3d_last_error()) > 0
 
     run()
+
+
+def test_select_engine_on_the_host():
+    """dmv3d_select_engine resolves AUTO without device work: fp32 storage -> SIMT; bf16
+    triplane + weights with hidden 64 and a workspace -> TCGEN05; an explicit TCGEN05
+    request the tensor cores cannot serve -> UNSUPPORTED (every documented activation
+    is accepted by the tensor-core engine's forward)."""
+    keep = []
+    t, c, m, o = _valid_structs(keep)
+    e = ct.c_int32(-1)
+    L = _abi.lib()
+    assert L.dmv3d_select_engine(ct.byref(t), ct.byref(m), ct.byref(o), 1, ct.byref(e)) == _abi.OK
+    assert e.value == _abi.ENGINE_SIMT
+    # a bf16 80-channel triplane with the paper's 80-64-64-64-4 MLP
+    tp = np.zeros((3, 4, 4, 80), np.uint16)
+    ws = [np.zeros((64, 80), np.uint16), np.zeros((64, 64), np.uint16), np.zeros((64, 64), np.uint16),
+          np.zeros((4, 64), np.uint16)]
+    bs = [np.zeros(64, np.float32)] * 3 + [np.zeros(4, np.float32)]
+    warr = (ct.c_void_p * 4)(*[w.ctypes.data for w in ws])
+    barr = (ct.c_void_p * 4)(*[b.ctypes.data for b in bs])
+    keep += [tp, ws, bs, warr, barr]
+    t2 = _abi.Triplane(4, 80, _abi.BF16, tp.ctypes.data, (ct.c_float * 3)(-1, -1, -1),
+                       (ct.c_float * 3)(1, 1, 1))
+    nbytes = 0
+    for act in (0, 1, 2):
+        m2 = _abi.MLP(4, 80, 64, _abi.BF16, ct.cast(warr, ct.POINTER(ct.c_void_p)),
+                      ct.cast(barr, ct.POINTER(ct.c_void_p)), act, 0.0, 0.0)
+        nbytes = L.dmv3d_workspace_bytes(ct.byref(t2), ct.byref(m2))
+        ws_buf = np.zeros(nbytes + 512, np.uint8)
+        keep.append(ws_buf)
+        o2 = _abi.RenderOpts(16, 0, 0, 0, (ct.c_float * 3)(1, 1, 1), 0.0, -1, -1, 0, None)
+        o2.workspace = (ws_buf.ctypes.data + 255) // 256 * 256
+        o2.workspace_bytes = nbytes
+        assert L.dmv3d_select_engine(ct.byref(t2), ct.byref(m2), ct.byref(o2), 1, ct.byref(e)) == _abi.OK
+        assert e.value == _abi.ENGINE_TCGEN05, act
+        o2.workspace = None  # no workspace: AUTO falls back, an explicit TCGEN05 fails
+        assert L.dmv3d_select_engine(ct.byref(t2), ct.byref(m2), ct.byref(o2), 1, ct.byref(e)) == _abi.OK
+        assert e.value == _abi.ENGINE_SIMT
+    assert nbytes > 0
+    o.engine = _abi.ENGINE_TCGEN05  # fp32 storage
+    assert L.dmv3d_select_engine(ct.byref(t), ct.byref(m), ct.byref(o), 1, ct.byref(e)) == _abi.ERR_UNSUPPORTED
+    assert L.dmv3d_select_engine(ct.byref(t), ct.byref(m), ct.byref(o), 1, None) == _abi.ERR_INVALID_ARG
+
+
+def test_range_flags_rejects_null():
+    out = ct.c_uint32()
+    assert _abi.lib().dmv3d_range_flags(None, ct.byref(out), None) == _abi.ERR_INVALID_ARG
+    assert _abi.lib().dmv3d_workspace_range_flags(None, ct.byref(out)) == _abi.ERR_INVALID_ARG
+
+
+def test_bench_reports_traffic_only_for_the_captured_kernel(tmp_path, monkeypatch):
+    """bench.py's roofline.traffic comes from an ncu capture stamped with the kernel source
+    sha: a capture of other sources is reported as stale (null), never silently reused."""
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    sha = bench.kernel_source_sha("tcgen05")
+    assert len(sha) == 16 and sha != bench.kernel_source_sha("simt")
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    (prof / "ncu_traffic.json").write_text(json.dumps({"tcgen05": 123, "tcgen05_source_sha": sha}))
+    monkeypatch.setattr(bench, "kernel_source_sha", lambda e: sha)
+    assert bench._ncu_traffic("tcgen05")[0] == 123
+    (prof / "ncu_traffic.json").write_text(json.dumps({"tcgen05": 123, "tcgen05_source_sha": "0" * 16}))
+    v, note = bench._ncu_traffic("tcgen05")
+    assert v is None and "stale" in note
