@@ -2,6 +2,7 @@
     compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize.py
 Tensor-core and SIMT renders (fused DDIM, ray range, tiles), backward on both engines,
 density grid on both engines, standalone DDIM, Plucker map, stage-level debug entries."""
+import os
 import sys
 
 import numpy as np
@@ -34,7 +35,24 @@ for dtype in ("bf16", "f32"):
                                   term_eps=1e-3, fwd=(rgb, alpha))
         api.dmv3d_density_grid(t, mlp, 13, engine=e)
     api.dmv3d_ddim_step(ab, 500, 480, x_t, rgb[:2].contiguous(), torch.randn_like(x_t), eta=0.5)
+    if dtype == "bf16":
+        # round 2: SiLU / softplus hidden layers on the tensor cores, range flags, batched step
+        for act in (1, 2):
+            m2 = wl.bf16_mlp(wl.blob_mlp(32, 64, 4, seed=3))
+            m2.hidden_act = act
+            api.dmv3d_render_views(t, intr, c2w, H, W, api.DeviceMLP.from_host(m2, "bf16", "cuda"),
+                                   samples_per_ray=N, engine="tcgen05")
+        api.dmv3d_range_flags()
+        tb = torch.stack([t, t]).contiguous()
+        xb = torch.stack([x_t, x_t]).contiguous()
+        api.dmv3d_render_ddim_step_batched(tb, torch.stack([intr, intr]), torch.stack([c2w, c2w]), H, W,
+                                           mlp, ab, 980, 960, xb, samples_per_ray=N, engine="tcgen05",
+                                           term_eps=1e-4)
 api.dmv3d_plucker_rays(intr, c2w, H, W)
+for rpt in ("1", "2", "4"):  # every store width of the Plucker kernel, with a cut ray range
+    os.environ["DMV3D_PLUCKER_RPT"] = rpt
+    api.dmv3d_plucker_rays(intr, c2w, H, W, ray_range=(8, 4 * H * W - 4))
+os.environ.pop("DMV3D_PLUCKER_RPT")
 pts = torch.rand((100, 3), device="cuda") * 2 - 1
 api.dmv3d_debug_sample_features(t, pts)
 api.dmv3d_debug_decode(t, mlp, pts)
