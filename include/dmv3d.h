@@ -193,7 +193,9 @@ uint64_t dmv3d_workspace_bytes(const dmv3d_triplane *triplane, const dmv3d_mlp *
  * hidden activations are fp16 MMA operands).  Reads the range flags of the last
  * TCGEN05 call that used `workspace` (enqueued on `stream`; this call synchronises the
  * stream): bit 0 = some G value was outside +-65504 (or NaN), bit 1 = some evaluated
- * sample's head output was not finite (an activation overflowed fp16).  Either bit
+ * sample's head output was not finite (an activation overflowed fp16; a weight of
+ * layers 1..L-1 beyond +-65504 becomes inf in its fp16 copy and shows up here too;
+ * weights below fp16's smallest subnormal, 6e-8, round to 0).  Either bit
  * means the call's outputs contain inf / NaN: rescale the triplane / weights or use
  * the SIMT engine (fp32).  0 = in range.  The flags are cleared by every call that
  * projects the triplane (each TCGEN05 render / DDIM / backward / grid call). */
