@@ -103,8 +103,9 @@ static size_t tc_smem_bytes(int L) {
 }
 
 // ------------------------------------------------------------------ K0
-// G[t][o] = fp16(sum_c F[t][c] W0[o][c] + b0[o] * bscale); one warp per texel,
-// lane -> outputs (2 lane, 2 lane + 1); W0 transposed in smem (conflict-free).
+// G[t][o] = fp16(sum_c F[t][c] W0[o][c] + b0[o] * bscale); one warp per 4 texels (bf16;
+// per texel for FP8), lane -> outputs (2 lane, 2 lane + 1); W0 transposed in smem
+// (conflict-free), each of its elements read once per 4 texels.
 // W0 rows have stride `wstride` (3 C for the concat aggregation, whose planes are
 // projected by their own column block of W0).  Optionally zeroes the patch counter
 // and writes fp16(b0) to `gbias` (the bias row of the half-pixel mode).
@@ -129,17 +130,17 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bias0 = __ldg(b0 + 2 * lane) * bscale, bias1 = __ldg(b0 + 2 * lane + 1) * bscale;
-  const int64_t t_first = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t t_step = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // bf16: lane q holds 16-B chunk q of the texel row (C <= 256: <= 32 chunks), loaded in
-  // one round trip and one texel ahead; the dot products read the chunks by shuffle
-  const int nq = FP8 ? 0 : C / 8;
-  uint4 cur = make_uint4(0u, 0u, 0u, 0u);
-  if (!FP8 && t_first < ntex && lane < nq)
-    cur = __ldg(reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(Fv) + t_first * C) + lane);
-  for (int64_t t = t_first; t < ntex; t += t_step) {
-    float a0 = bias0, a1 = bias1;
-    if constexpr (FP8) {
+  const int64_t w_first = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t w_step = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // stores G[t] (this lane's output pair), with the fp16 range guard: G outside +-65504
+  // (or NaN) raises range flag bit 0; the value is stored as inf / NaN (no silent clamp)
+  auto store = [&](int64_t t, float a0, float a1) {
+    if (!(fabsf(a0) <= 65504.0f && fabsf(a1) <= 65504.0f)) atomicOr(range_flags, 1u);
+    const int64_t ta = t / per_asset;  // asset: its G block has one extra (bias) row
+    reinterpret_cast<uint32_t *>(G + (t + ta) * kTcHD)[lane] = ptx::pack_f16x2(a0, a1);
+  };
+  if constexpr (FP8) {
+    for (int64_t t = w_first; t < ntex; t += w_step) {
       const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint8_t *>(Fv) + t * C);
       float s0 = 0.0f, s1 = 0.0f;
       for (int q = 0; q < C / 16; ++q) {
@@ -156,38 +157,47 @@ __global__ void __launch_bounds__(256)
           s1 += w0.y * f.x + w1.y * f.y;
         }
       }
-      a0 += fscale * s0;
-      a1 += fscale * s1;
-    } else {
-      const int64_t tn = t + t_step;
-      uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
-      if (tn < ntex && lane < nq)
-        nxt = __ldg(reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(Fv) + tn * C) + lane);
-      float b0s = 0.0f, b1s = 0.0f;  // second pair of partial sums: two chains per output
+      store(t, bias0 + fscale * s0, bias1 + fscale * s1);
+    }
+  } else {
+    // bf16: a warp projects kTexW texels per iteration, so every W0 element it reads from
+    // shared memory serves kTexW texels (shared-memory bound otherwise); lane q holds
+    // 16-B chunk q of each texel row (C <= 256: <= 32 chunks), read by shuffle
+    constexpr int kTexW = 4;
+    const int nq = C / 8;
+    const __nv_bfloat16 *F = static_cast<const __nv_bfloat16 *>(Fv);
+    for (int64_t tg = w_first; tg * kTexW < ntex; tg += w_step) {
+      uint4 cur[kTexW];
+#pragma unroll
+      for (int u = 0; u < kTexW; ++u) {
+        const int64_t t = tg * kTexW + u;
+        cur[u] = (t < ntex && lane < nq) ? __ldg(reinterpret_cast<const uint4 *>(F + t * C) + lane)
+                                         : make_uint4(0u, 0u, 0u, 0u);
+      }
+      float a0[kTexW], a1[kTexW];
+#pragma unroll
+      for (int u = 0; u < kTexW; ++u) a0[u] = a1[u] = 0.0f;
       for (int q = 0; q < nq; ++q) {
-        const uint32_t uv[4] = {__shfl_sync(0xffffffffu, cur.x, q), __shfl_sync(0xffffffffu, cur.y, q),
-                                __shfl_sync(0xffffffffu, cur.z, q), __shfl_sync(0xffffffffu, cur.w, q)};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 w0 = swt[(q * 8 + 2 * e) * (kTcHD / 2) + lane];
           const float2 w1 = swt[(q * 8 + 2 * e + 1) * (kTcHD / 2) + lane];
-          const float f0 = bf16lo(uv[e]), f1 = bf16hi(uv[e]);
-          a0 += w0.x * f0;
-          a1 += w0.y * f0;
-          b0s += w1.x * f1;
-          b1s += w1.y * f1;
+#pragma unroll
+          for (int u = 0; u < kTexW; ++u) {
+            const uint32_t word = __shfl_sync(0xffffffffu, e == 0 ? cur[u].x : e == 1 ? cur[u].y
+                                                           : e == 2 ? cur[u].z : cur[u].w, q);
+            const float f0 = bf16lo(word), f1 = bf16hi(word);
+            a0[u] += w0.x * f0 + w1.x * f1;
+            a1[u] += w0.y * f0 + w1.y * f1;
+          }
         }
       }
-      a0 += b0s;
-      a1 += b1s;
-      cur = nxt;
+#pragma unroll
+      for (int u = 0; u < kTexW; ++u) {
+        const int64_t t = tg * kTexW + u;
+        if (t < ntex) store(t, bias0 + a0[u], bias1 + a1[u]);
+      }
     }
-    // fp16 range guard: G outside +-65504 (or NaN) raises range flag bit 0; the value is
-    // stored as inf / NaN (no silent clamp), so the affected outputs are non-finite
-    if (!(fabsf(a0) <= 65504.0f && fabsf(a1) <= 65504.0f)) atomicOr(range_flags, 1u);
-    const uint32_t pk = ptx::pack_f16x2(a0, a1);
-    const int64_t ta = t / per_asset;  // asset: its G block has one extra (bias) row
-    reinterpret_cast<uint32_t *>(G + (t + ta) * kTcHD)[lane] = pk;
   }
 }
 
@@ -776,22 +786,22 @@ cudaError_t launch_preproject(const RenderParams &P, cudaStream_t st) {
   const size_t esz = P.tp_fp8 ? 1 : 2;
   const __nv_bfloat16 *W0 = reinterpret_cast<const __nv_bfloat16 *>(P.w[0]);
   const bool cat = P.agg == 2;
-#ifndef DMV3D_K0_BLOCKS_PER_SM
-#define DMV3D_K0_BLOCKS_PER_SM 2  // fewer blocks: each loads W0 (20 KiB) once; 8 measured 1 % slower on cfg2
-#endif
+  // blocks per SM: 2 for a paper-sized triplane (each block loads W0, 20 KiB, once; 8
+  // measured 1 % slower on cfg2), 4 (the register limit) for large / batched triplanes
+  auto k0_blocks = [&](int64_t texels) { return texels > (int64_t)64 * 1024 ? 4 : 2; };
   const size_t gs = ((size_t)ntex + 1) * kTcHD;  // G block of one asset
   if (!cat) {  // all assets' texels in one launch
     const int64_t nt = (int64_t)A * ntex;
-    int64_t g0 = (nt * 32 + 255) / 256;
-    if (g0 > sms * DMV3D_K0_BLOCKS_PER_SM) g0 = sms * DMV3D_K0_BLOCKS_PER_SM;
+    int64_t g0 = (nt * 8 + 255) / 256;  // one warp per 4 texels
+    if (g0 > (int64_t)sms * k0_blocks(nt)) g0 = (int64_t)sms * k0_blocks(nt);
     kern<<<(int)g0, 256, s0, st>>>(F, (int)nt, P.C, P.C, W0, P.b[0], bscale, P.tp_scale, G, counter,
                                    G + (size_t)ntex * kTcHD, ntex, A, counter + 1);
     return cudaGetLastError();
   }
   // concat: plane p of every asset is projected by its own column block of W0
   const int nt = P.R * P.R;
-  int g0 = (nt * 32 + 255) / 256;
-  if (g0 > sms * DMV3D_K0_BLOCKS_PER_SM) g0 = sms * DMV3D_K0_BLOCKS_PER_SM;
+  int g0 = (nt * 8 + 255) / 256;
+  if (g0 > sms * k0_blocks(nt)) g0 = sms * k0_blocks(nt);
   for (int a = 0; a < A; ++a)
     for (int pl = 0; pl < 3; ++pl) {
       const bool first = a == 0 && pl == 0;
