@@ -348,6 +348,25 @@ dmv3d_status dmv3d_render_ddim_step_host(dmv3d_workspace *ws, const dmv3d_tripla
                                          const float *z, float *x_prev, float *rgb,
                                          float *alpha, dmv3d_stream stream);
 
+/* Interleaved-tile merge (opts.tile_size / tile_rank / tile_count).  Packed
+ * layout: rank r's k-th tile (tile id tau = r + k world over the whole camera set, the
+ * ids of the tile formula above) is block k of that rank's rgb [nmax][3][T][T], alpha
+ * [nmax][T][T] and x_prev [nmax][3][T][T], nmax = ceil(tiles / world) (a rank's blocks
+ * past its last tile are unused; x_prev blocks only for views < ddim_views).
+ * dmv3d_tiles_pack copies rank `rank`'s tiles from image-layout rgb [V][3][H][W], alpha
+ * [V][H][W], x_prev [ddim_views][3][H][W] (a tile-sharded render's outputs) into its
+ * blocks; after the ranks' blocks are all-gathered back to back ([world][nmax]...),
+ * dmv3d_tiles_unpack scatters every rank's blocks into the images.  Any of the three
+ * (image, packed) pairs may be NULL.  Async on `stream`; one HBM-bound pass each. */
+dmv3d_status dmv3d_tiles_pack(const dmv3d_cameras *cams, int32_t tile_size, int32_t rank, int32_t world,
+                              int32_t ddim_views, const float *rgb, const float *alpha,
+                              const float *x_prev, float *packed_rgb, float *packed_alpha,
+                              float *packed_x_prev, dmv3d_stream stream);
+dmv3d_status dmv3d_tiles_unpack(const dmv3d_cameras *cams, int32_t tile_size, int32_t world,
+                                int32_t ddim_views, const float *packed_rgb,
+                                const float *packed_alpha, const float *packed_x_prev,
+                                float *rgb, float *alpha, float *x_prev, dmv3d_stream stream);
+
 /* Thread-local message describing the last non-OK status ("" if none). */
 const char *dmv3d_last_error(void);
 /* Library version string. */

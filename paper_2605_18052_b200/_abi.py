@@ -28,6 +28,7 @@ EXPORTED = [
     "dmv3d_plucker_rays", "dmv3d_density_grid", "dmv3d_render_backward",
     "dmv3d_render_views_batched", "dmv3d_render_ddim_step_batched", "dmv3d_workspace_bytes_batched",
     "dmv3d_range_flags", "dmv3d_workspace_range_flags", "dmv3d_select_engine",
+    "dmv3d_tiles_pack", "dmv3d_tiles_unpack",
 ]
 
 
@@ -132,6 +133,12 @@ def lib() -> ct.CDLL:
         L.dmv3d_timer_reset.argtypes = [ct.c_void_p]
         L.dmv3d_timer_read.argtypes = [ct.c_void_p, P(ct.c_double), P(ct.c_int64)]
         L.dmv3d_range_flags.argtypes = [ct.c_void_p, P(ct.c_uint32), ct.c_void_p]
+        L.dmv3d_tiles_unpack.argtypes = [P(Cameras), ct.c_int32, ct.c_int32, ct.c_int32, ct.c_void_p,
+                                         ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                         ct.c_void_p, ct.c_void_p]
+        L.dmv3d_tiles_pack.argtypes = [P(Cameras), ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32,
+                                       ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                       ct.c_void_p, ct.c_void_p, ct.c_void_p]
         L.dmv3d_workspace_range_flags.argtypes = [ct.c_void_p, P(ct.c_uint32)]
         L.dmv3d_select_engine.argtypes = [P(Triplane), P(MLP), P(RenderOpts), ct.c_int32,
                                           P(ct.c_int32)]

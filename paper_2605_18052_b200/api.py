@@ -171,6 +171,36 @@ def dmv3d_plucker_rays(intrinsics, c2w, height, width, out=None, ray_range=None)
     return out
 
 
+def tiles_per_rank(num_views, height, width, tile, world):
+    """Blocks per rank of the tile-packed layout: ceil(tiles / world)."""
+    ntiles = num_views * -(-height // tile) * -(-width // tile)
+    return -(-ntiles // world)
+
+
+def dmv3d_tiles_pack(intrinsics, c2w, height, width, tile, rank, world, rgb=None, alpha=None,
+                     x_prev=None, packed_rgb=None, packed_alpha=None, packed_x_prev=None,
+                     ddim_views=0):
+    """Copy rank `rank`'s interleaved tiles from image-layout outputs into its packed
+    blocks (rgb [nmax,3,T,T], alpha [nmax,T,T], x_prev [nmax,3,T,T])."""
+    c = cameras_struct(intrinsics, c2w, height, width)
+    _abi.check(_abi.lib().dmv3d_tiles_pack(ct.byref(c), int(tile), int(rank), int(world),
+                                           int(ddim_views), _ptr(rgb), _ptr(alpha), _ptr(x_prev),
+                                           _ptr(packed_rgb), _ptr(packed_alpha),
+                                           _ptr(packed_x_prev), _stream(c2w.device)))
+
+
+def dmv3d_tiles_unpack(intrinsics, c2w, height, width, tile, world, packed_rgb=None,
+                       packed_alpha=None, packed_x_prev=None, rgb=None, alpha=None, x_prev=None,
+                       ddim_views=0):
+    """Scatter `world` ranks' gathered tile-packed outputs ([world * tiles_per_rank, ...])
+    into image-layout rgb [V,3,H,W], alpha [V,H,W], x_prev [ddim_views,3,H,W]."""
+    c = cameras_struct(intrinsics, c2w, height, width)
+    _abi.check(_abi.lib().dmv3d_tiles_unpack(ct.byref(c), int(tile), int(world), int(ddim_views),
+                                             _ptr(packed_rgb), _ptr(packed_alpha),
+                                             _ptr(packed_x_prev), _ptr(rgb), _ptr(alpha),
+                                             _ptr(x_prev), _stream(c2w.device)))
+
+
 class Timer:
     """dmv3d_timer: CUDA events the library records around each render kernel."""
 

@@ -136,6 +136,7 @@ dmv3d_status check_opts(const dmv3d_render_opts *o, int64_t nrays) {
   CHECK_ARG(all || (o->ray_begin >= 0 && o->ray_begin <= o->ray_end && o->ray_end <= nrays),
             "opts: ray range must be -1,-1 or 0 <= begin <= end <= V*H*W");
   if (o->counters) CHECK_ALIGN(o->counters, "opts.counters");
+
   if (o->workspace && (reinterpret_cast<uintptr_t>(o->workspace) & 255u))
     return fail(DMV3D_ERR_ALIGNMENT, "opts.workspace is not 256-byte aligned");
   CHECK_ARG(o->num_peers >= 0 && o->num_peers <= kMaxPeers, "opts: num_peers must be in [0, 7]");
@@ -200,6 +201,7 @@ void fill_common(RenderParams &P, const dmv3d_triplane *t, const dmv3d_cameras *
     P.tile_size = o->tile_size;
     P.tile_rank = o->tile_rank;
     P.tile_count = o->tile_count > 0 ? o->tile_count : 1;
+
     for (int k = 0; k < o->num_peers; ++k) {
       P.peer_rgb[k] = o->peer_rgb ? o->peer_rgb[k] : nullptr;
       P.peer_alpha[k] = o->peer_alpha ? o->peer_alpha[k] : nullptr;
@@ -772,6 +774,50 @@ dmv3d_status dmv3d_workspace_destroy(dmv3d_workspace *ws) {
   }
   delete ws;
   return DMV3D_OK;
+}
+
+static dmv3d_status check_tiles(const dmv3d_cameras *cams, int32_t tile_size, int32_t world,
+                                int32_t ddim_views, const float *a0, const float *a1, const float *b0,
+                                const float *b1, const float *c0, const float *c1) {
+  CHECK_ARG(cams != nullptr, "cameras is NULL");
+  CHECK_ARG(cams->num_views >= 1 && cams->height >= 1 && cams->width >= 1, "cameras: V, H, W must be >= 1");
+  CHECK_ARG(tile_size > 0 && tile_size % 4 == 0, "tiles: tile_size must be a positive multiple of 4");
+  CHECK_ARG(world >= 1, "tiles: world must be >= 1");
+  CHECK_ARG((a0 == nullptr) == (a1 == nullptr) && (b0 == nullptr) == (b1 == nullptr) &&
+                (c0 == nullptr) == (c1 == nullptr),
+            "tiles: packed / image buffers must be given in pairs");
+  CHECK_ARG(c0 == nullptr || (ddim_views >= 1 && ddim_views <= cams->num_views),
+            "tiles: need 1 <= ddim_views <= V for x_prev");
+  return DMV3D_OK;
+}
+
+dmv3d_status dmv3d_tiles_pack(const dmv3d_cameras *cams, int32_t tile_size, int32_t rank, int32_t world,
+                              int32_t ddim_views, const float *rgb, const float *alpha,
+                              const float *x_prev, float *packed_rgb, float *packed_alpha,
+                              float *packed_x_prev, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s = check_tiles(cams, tile_size, world, ddim_views, rgb, packed_rgb, alpha, packed_alpha,
+                               x_prev, packed_x_prev);
+  if (s != DMV3D_OK) return s;
+  CHECK_ARG(rank >= 0 && rank < world, "tiles_pack: need 0 <= rank < world");
+  return cuda_status(launch_tiles_copy(cams->num_views, cams->height, cams->width, tile_size, rank, world,
+                                       ddim_views, true, rgb, alpha, x_prev, packed_rgb, packed_alpha,
+                                       packed_x_prev, reinterpret_cast<cudaStream_t>(stream)),
+                     "tiles_pack launch");
+}
+
+dmv3d_status dmv3d_tiles_unpack(const dmv3d_cameras *cams, int32_t tile_size, int32_t world,
+                                int32_t ddim_views, const float *packed_rgb,
+                                const float *packed_alpha, const float *packed_x_prev,
+                                float *rgb, float *alpha, float *x_prev, dmv3d_stream stream) {
+  g_err.clear();
+  dmv3d_status s = check_tiles(cams, tile_size, world, ddim_views, packed_rgb, rgb, packed_alpha, alpha,
+                               packed_x_prev, x_prev);
+  if (s != DMV3D_OK) return s;
+  return cuda_status(launch_tiles_copy(cams->num_views, cams->height, cams->width, tile_size, -1, world,
+                                       ddim_views, false, packed_rgb, packed_alpha, packed_x_prev, rgb,
+                                       alpha, x_prev, reinterpret_cast<cudaStream_t>(stream)),
+                     "tiles_unpack launch");
 }
 
 dmv3d_status dmv3d_range_flags(const void *workspace, uint32_t *flags, dmv3d_stream stream) {

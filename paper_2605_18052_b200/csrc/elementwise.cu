@@ -283,6 +283,65 @@ cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Interleaved-tile merge.  Packed layout: rank r's k-th tile (tile id
+// r + k world over the whole camera set) is block r nmax + k of rgb [.][3][T][T], alpha
+// [.][T][T], x_prev [.][3][T][T] (pack writes one rank's blocks 0..nmax-1 of its own
+// buffer, unpack reads all ranks' blocks).  One thread per packed pixel.
+__global__ void __launch_bounds__(256) tiles_copy_kernel(int V, int H, int W, int T, int rank, int world,
+                                                         int64_t nmax, int ddim_views, int pack,
+                                                         const float *__restrict__ s_rgb,
+                                                         const float *__restrict__ s_alpha,
+                                                         const float *__restrict__ s_xp, float *d_rgb,
+                                                         float *d_alpha, float *d_xp) {
+  const int64_t TT = (int64_t)T * T, HW = (int64_t)H * W;
+  const int64_t TH = (H + T - 1) / T, TW = (W + T - 1) / T, ntiles = (int64_t)V * TH * TW;
+  const int64_t nranks = pack ? 1 : world;
+  const int64_t total = nranks * nmax * TT;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = e / TT, pp = e - blk * TT;
+    const int64_t r = pack ? rank : blk / nmax, k = pack ? blk : blk - r * nmax;
+    const int64_t tau = r + k * world;
+    if (tau >= ntiles) continue;
+    const int v = (int)(tau / (TH * TW));
+    const int64_t trem = tau - (int64_t)v * TH * TW;
+    const int i = (int)(trem / TW) * T + (int)(pp / T), j = (int)(trem % TW) * T + (int)(pp % T);
+    if (i >= H || j >= W) continue;
+    const int64_t pix = (int64_t)i * W + j;
+    const int64_t ia = (int64_t)v * HW + pix, pa = blk * TT + pp;
+    if (s_alpha) {
+      if (pack) d_alpha[pa] = __ldg(s_alpha + ia);
+      else d_alpha[ia] = __ldg(s_alpha + pa);
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const int64_t img = ((int64_t)v * 3 + ch) * HW + pix, pk = (blk * 3 + ch) * TT + pp;
+      if (s_rgb) {
+        if (pack) d_rgb[pk] = __ldg(s_rgb + img);
+        else d_rgb[img] = __ldg(s_rgb + pk);
+      }
+      if (s_xp && v < ddim_views) {
+        if (pack) d_xp[pk] = __ldg(s_xp + img);
+        else d_xp[img] = __ldg(s_xp + pk);
+      }
+    }
+  }
+}
+
+cudaError_t launch_tiles_copy(int V, int H, int W, int T, int rank, int world, int ddim_views, bool pack,
+                              const float *src_rgb, const float *src_alpha, const float *src_xp,
+                              float *dst_rgb, float *dst_alpha, float *dst_xp, cudaStream_t st) {
+  const int64_t TH = (H + T - 1) / T, TW = (W + T - 1) / T, ntiles = (int64_t)V * TH * TW;
+  const int64_t nmax = (ntiles + world - 1) / world;
+  const int64_t total = (pack ? 1 : (int64_t)world) * nmax * T * T;
+  if (total <= 0) return cudaSuccess;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  tiles_copy_kernel<<<(int)grid, 256, 0, st>>>(V, H, W, T, rank, world, nmax, ddim_views, pack ? 1 : 0,
+                                               src_rgb, src_alpha, src_xp, dst_rgb, dst_alpha, dst_xp);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
                                 cudaStream_t st) {
   const int64_t n = P.ray_end - P.ray_begin;

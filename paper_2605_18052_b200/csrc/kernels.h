@@ -61,6 +61,11 @@ cudaError_t launch_ddim(const DdimCoef &c, int V, int H, int W, const float *x_t
                         const float *x0_rgb, const float *z, const uint8_t *keep_dev,
                         float *x_prev, cudaStream_t st);
 cudaError_t launch_plucker(const RenderParams &P, float *out, cudaStream_t st);
+// interleaved-tile merge: pack (rank's tiles, image -> blocks) or unpack (every rank's
+// gathered blocks -> images); src / dst are (rgb, alpha, x_prev) triples
+cudaError_t launch_tiles_copy(int V, int H, int W, int T, int rank, int world, int ddim_views, bool pack,
+                              const float *src_rgb, const float *src_alpha, const float *src_xp,
+                              float *dst_rgb, float *dst_alpha, float *dst_xp, cudaStream_t st);
 cudaError_t launch_ray_geometry(const RenderParams &P, float *o_d, float *tn_tf, uint8_t *hit,
                                 cudaStream_t st);
 cudaError_t launch_sample_points(const RenderParams &P, float *t_k, float *points,

@@ -16,8 +16,10 @@ in the priority order of §8e:
   views are whole 4x4-patch rows, so the result is bitwise the one-GPU step (P12).
 * interleaved ray tiles (`denoise_step_tile_sharded`): the T x T tiles
   tau = (v ceil(H/T) + i/T) ceil(W/T) + j/T with tau mod P == rank (opts.tile_*),
-  which spreads AABB misses and early-terminated rays evenly.  Merged by one
-  all-reduce (every pixel has exactly one non-zero writer), or -- the fused form --
+  which spreads AABB misses and early-terminated rays evenly.  Each rank packs its
+  tiles block by block (`dmv3d_tiles_pack`); one coalesced all-gather of the packed
+  blocks and `dmv3d_tiles_unpack` assemble the images (`packed=False`: zeroed full-size
+  outputs merged by one all-reduce, ~2x the bytes), or -- the fused form --
 * `p2p=True` (views or tiles): the outputs live in symmetric memory
   (torch.distributed._symmetric_memory) and the render epilogue itself stores every
   value into all peers' buffers over NVLink (opts.peers of the ABI), so the exchange
@@ -219,12 +221,30 @@ def denoise_step_view_sharded(triplane, intrinsics, c2w, height, width, mlp, alp
 
 
 # ------------------------------------------------------------------ tiles
+def default_pack_fn(intrinsics, c2w, height, width, tile, rank, world, rgb, alpha, xp, prgb,
+                    palpha, pxp, ddim_views):
+    from . import api
+    api.dmv3d_tiles_pack(intrinsics, c2w, height, width, tile, rank, world, rgb, alpha, xp, prgb,
+                         palpha, pxp, ddim_views)
+
+
+def default_unpack_fn(intrinsics, c2w, height, width, tile, world, prgb, palpha, pxp, rgb, alpha,
+                      xp, ddim_views):
+    from . import api
+    api.dmv3d_tiles_unpack(intrinsics, c2w, height, width, tile, world, prgb, palpha, pxp, rgb,
+                           alpha, xp, ddim_views)
+
+
 def denoise_step_tile_sharded(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev,
                               x_t, ddim_views: int, group=None, src: int = 0,
                               broadcast_triplane: bool = True, render_fn=None, tile: int = 16,
-                              p2p: bool = False, asset: PackedAsset | None = None, **opts):
+                              p2p: bool = False, asset: PackedAsset | None = None,
+                              packed: bool = True, pack_fn=None, unpack_fn=None, **opts):
     """One denoising step of one asset, T x T ray tiles dealt round robin to the ranks.
-    Returns the full (x_prev, rgb, alpha) on every rank.  `p2p`: outputs in symmetric
+    Returns the full (x_prev, rgb, alpha) on every rank.  `packed` (default): the rank's
+    tiles packed (`pack_fn`, default dmv3d_tiles_pack), one all-gather, unpacked
+    (`unpack_fn`, default dmv3d_tiles_unpack); `packed=False`: zeroed full-size outputs
+    and one all-reduce.  `p2p`: outputs in symmetric
     memory, every rank's render epilogue stores its pixels into all peers' buffers at the
     same offsets (no collective on the data path; one device-side barrier; views valid
     until the call after next)."""
@@ -247,6 +267,30 @@ def denoise_step_tile_sharded(triplane, intrinsics, c2w, height, width, mlp, alp
         ha.barrier()
         return xp[:ddim_views], rgb, alpha
     HW = height * width
+    if packed:
+        # the rank renders its tiles into image-layout scratch, dmv3d_tiles_pack copies them
+        # into its blocks (rgb [k][3][T][T], alpha [k][T][T], x_prev [k][3][T][T]), one
+        # coalesced all-gather stacks the ranks' blocks, dmv3d_tiles_unpack scatters them
+        pack_fn = pack_fn or default_pack_fn
+        unpack_fn = unpack_fn or default_unpack_fn
+        xp = torch.empty((ddim_views, 3, height, width), device=dev, dtype=torch.float32)
+        rgb = torch.empty((V, 3, height, width), device=dev, dtype=torch.float32)
+        alpha = torch.empty((V, height, width), device=dev, dtype=torch.float32)
+        render_fn(triplane, intrinsics, c2w, height, width, mlp, alpha_bar, t, t_prev, x_t, xp, rgb,
+                  alpha, tiles=(tile, rank, world), **opts)
+        if world == 1:
+            return xp, rgb, alpha
+        nmax = -(-(V * -(-height // tile) * -(-width // tile)) // world)
+        g_rgb = torch.empty((world * nmax, 3, tile, tile), device=dev, dtype=torch.float32)
+        g_a = torch.empty((world * nmax, tile, tile), device=dev, dtype=torch.float32)
+        g_x = torch.empty((world * nmax, 3, tile, tile), device=dev, dtype=torch.float32)
+        blk = slice(rank * nmax, (rank + 1) * nmax)
+        pack_fn(intrinsics, c2w, height, width, tile, rank, world, rgb, alpha, xp, g_rgb[blk], g_a[blk],
+                g_x[blk], ddim_views)
+        _all_gather_blocks([(g_rgb, g_rgb[blk]), (g_a, g_a[blk]), (g_x, g_x[blk])], group)
+        unpack_fn(intrinsics, c2w, height, width, tile, world, g_rgb, g_a, g_x, rgb, alpha, xp,
+                  ddim_views)
+        return xp, rgb, alpha
     n_x, n_rgb = ddim_views * 3 * HW, V * 3 * HW
     flat = torch.zeros(n_x + n_rgb + V * HW, device=dev, dtype=torch.float32)  # one collective
     xp = flat[:n_x].view(ddim_views, 3, height, width)

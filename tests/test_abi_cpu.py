@@ -271,3 +271,18 @@ def test_bench_reports_traffic_only_for_the_captured_kernel(tmp_path, monkeypatc
     (prof / "ncu_traffic.json").write_text(json.dumps({"tcgen05": 123, "tcgen05_source_sha": "0" * 16}))
     v, note = bench._ncu_traffic("tcgen05")
     assert v is None and "stale" in note
+
+
+def test_tiles_unpack_validation():
+    keep = []
+    t, c, m, o = _valid_structs(keep)
+    L = _abi.lib()
+    buf = np.zeros(64, np.float32)
+    assert L.dmv3d_tiles_unpack(ct.byref(c), 6, 2, 1, None, None, None, None, None, None, None) \
+        == _abi.ERR_INVALID_ARG  # tile size not a multiple of 4
+    assert L.dmv3d_tiles_unpack(ct.byref(c), 4, 0, 1, None, None, None, None, None, None, None) \
+        == _abi.ERR_INVALID_ARG  # world
+    assert L.dmv3d_tiles_unpack(ct.byref(c), 4, 2, 1, buf.ctypes.data, None, None, None, None, None,
+                                None) == _abi.ERR_INVALID_ARG  # unpaired buffers
+    assert L.dmv3d_tiles_pack(ct.byref(c), 4, 2, 2, 1, None, None, None, None, None, None, None) \
+        == _abi.ERR_INVALID_ARG  # rank >= world

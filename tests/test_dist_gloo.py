@@ -71,7 +71,44 @@ def _oracle_tile_render_fn(triplane, intrinsics, c2w, H, W, mlp, alpha_bar, t, t
                         x_prev[v, :, i, j] = full_x[v, :, i, j]
 
 
-def _tile_worker(rank, world, port, out_dir):
+def _tile_blocks(V, H, W, T, world):
+    """(rank, block k, view, tile row, tile col) of every tile, from the tile formula
+    tau = (v th + i / T) tw + j / T written out here: rank tau mod P, block tau div P."""
+    th, tw = -(-H // T), -(-W // T)
+    for tau in range(V * th * tw):
+        v, rem = divmod(tau, th * tw)
+        yield tau % world, tau // world, v, rem // tw, rem % tw
+
+
+def _loop_pack_fn(intrinsics, c2w, H, W, T, rank, world, rgb, alpha, xp, prgb, palpha, pxp, ddim_views):
+    for r, k, v, ti, tj in _tile_blocks(c2w.shape[0], H, W, T, world):
+        if r != rank:
+            continue
+        for pi in range(T):
+            for pj in range(T):
+                i, j = ti * T + pi, tj * T + pj
+                if i < H and j < W:
+                    prgb[k, :, pi, pj] = rgb[v, :, i, j]
+                    palpha[k, pi, pj] = alpha[v, i, j]
+                    if v < ddim_views:
+                        pxp[k, :, pi, pj] = xp[v, :, i, j]
+
+
+def _loop_unpack_fn(intrinsics, c2w, H, W, T, world, prgb, palpha, pxp, rgb, alpha, xp, ddim_views):
+    nmax = prgb.shape[0] // world
+    for r, k, v, ti, tj in _tile_blocks(c2w.shape[0], H, W, T, world):
+        b = r * nmax + k
+        for pi in range(T):
+            for pj in range(T):
+                i, j = ti * T + pi, tj * T + pj
+                if i < H and j < W:
+                    rgb[v, :, i, j] = prgb[b, :, pi, pj]
+                    alpha[v, i, j] = palpha[b, pi, pj]
+                    if v < ddim_views:
+                        xp[v, :, i, j] = pxp[b, :, pi, pj]
+
+
+def _tile_worker(rank, world, port, out_dir, packed=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -82,16 +119,18 @@ def _tile_worker(rank, world, port, out_dir):
         xp, rgb, alpha = pdist.denoise_step_tile_sharded(
             triplane, torch.from_numpy(cams.intrinsics), torch.from_numpy(cams.c2w), 6, 5, m,
             schedule.cosine_alpha_bar(), 980, 960, x_t, ddim_views=3,
-            render_fn=_oracle_tile_render_fn, tile=4, samples_per_ray=16)
+            render_fn=_oracle_tile_render_fn, tile=4, samples_per_ray=16, packed=packed,
+            pack_fn=_loop_pack_fn, unpack_fn=_loop_unpack_fn)
         np.savez(os.path.join(out_dir, f"t{rank}.npz"), xp=xp.numpy(), rgb=rgb.numpy(),
                  alpha=alpha.numpy())
     finally:
         dist.destroy_process_group()
 
 
-def test_tile_sharded_step_matches_single_process(tmp_path):
+@pytest.mark.parametrize("packed", [True, False], ids=["all-gather", "all-reduce"])
+def test_tile_sharded_step_matches_single_process(tmp_path, packed):
     world = 2
-    mp.spawn(_tile_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_tile_worker, args=(world, _free_port(), str(tmp_path), packed), nprocs=world, join=True)
     import oracle
     tp, m, cams = _workload()
     orgb, oalpha = oracle.render_views(tp, cams, m, 16, threads=1)

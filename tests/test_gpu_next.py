@@ -5,7 +5,7 @@ import pytest
 import torch
 
 import oracle
-from paper_2605_18052_b200 import api
+from paper_2605_18052_b200 import api, schedule
 from paper_2605_18052_b200 import workloads as wl
 
 from helpers import dev_cams, dev_workload
@@ -273,3 +273,42 @@ def test_tiles_with_peer_stores(engine, dtype):
             assert torch.equal(pa[k][mine], alpha[mine]) and (pa[k][~mine] == -7.0).all()
             m3 = mine.unsqueeze(1).expand_as(rgb)
             assert torch.equal(pr[k][m3], rgb[m3]) and (pr[k][~m3] == -7.0).all()
+
+
+@pytest.mark.parametrize("engine,dtype", [("simt", "f32"), ("tcgen05", "bf16")])
+def test_tiles_packed_all_gather_is_the_one_gpu_step(engine, dtype):
+    """The interleaved-tile split merged by an all-gather of packed tiles: P emulated ranks
+    render their tiles (fused DDIM, eta = 1 with z, a keep-mask) and dmv3d_tiles_pack
+    copies them into their blocks, stacked rank by rank as the all-gather would;
+    dmv3d_tiles_unpack scatters them back: bitwise the one-GPU step, on a ragged image
+    (edge tiles) -- and through dist.denoise_step_tile_sharded in one process (world 1)."""
+    from paper_2605_18052_b200 import dist as pdist
+    tp = wl.blob_triplane(12, 32, seed=2)
+    m = wl.blob_mlp(32, 64, 4, seed=3)
+    if dtype == "bf16":
+        tp, m = wl.round_to_bf16(tp), wl.bf16_mlp(m)
+    H, W, T, P, DV = 21, 18, 8, 3, 2
+    cams = wl.concat_cameras(wl.input_cameras(H, W, 2), wl.novel_cameras(H, W, 2, seed=4))
+    t, intr, c2w, mlp = dev_workload(wl.Workload("tpk", tp, cams, m, 16, dtype))
+    ab = schedule.cosine_alpha_bar()
+    x_t = torch.from_numpy(wl.gaussian((DV, 3, H, W), 4)).cuda()
+    z = torch.from_numpy(wl.gaussian((DV, 3, H, W), 5)).cuda()
+    kw = dict(samples_per_ray=16, engine=engine, eta=1.0, z=z, keep_mask=[0, 1], term_eps=1e-4)
+    xp, rgb, alpha = api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, ab, 500, 480, x_t, **kw)
+    nmax = api.tiles_per_rank(4, H, W, T, P)
+    g_rgb = torch.full((P * nmax, 3, T, T), -7.0, device="cuda")
+    g_a = torch.full((P * nmax, T, T), -7.0, device="cuda")
+    g_x = torch.full((P * nmax, 3, T, T), -7.0, device="cuda")
+    for r in range(P):
+        sx, sr, sa = torch.empty_like(xp), torch.empty_like(rgb), torch.empty_like(alpha)
+        api.dmv3d_render_ddim_step(t, intr, c2w, H, W, mlp, ab, 500, 480, x_t, x_prev=sx, rgb=sr,
+                                   alpha=sa, tiles=(T, r, P), **kw)
+        b = slice(r * nmax, (r + 1) * nmax)
+        api.dmv3d_tiles_pack(intr, c2w, H, W, T, r, P, sr, sa, sx, g_rgb[b], g_a[b], g_x[b], DV)
+    urgb, ualpha = torch.full_like(rgb, -9.0), torch.full_like(alpha, -9.0)
+    uxp = torch.full_like(xp, -9.0)
+    api.dmv3d_tiles_unpack(intr, c2w, H, W, T, P, g_rgb, g_a, g_x, urgb, ualpha, uxp, DV)
+    assert torch.equal(urgb, rgb) and torch.equal(ualpha, alpha) and torch.equal(uxp, xp)
+    xp1, rgb1, alpha1 = pdist.denoise_step_tile_sharded(t, intr, c2w, H, W, mlp, ab, 500, 480, x_t, DV,
+                                                        tile=T, **kw)
+    assert torch.equal(rgb1, rgb) and torch.equal(alpha1, alpha) and torch.equal(xp1, xp)
