@@ -503,7 +503,7 @@ def main():
                                  "from HBM each step",
                            "parallelism": (f"16x16 ray tiles interleaved x{world} (packed triplane+MLP broadcast "
                                            + ("+ NVLink peer stores)" if args.mode == "tiles-p2p"
-                                              else "+ all-reduce)")
+                                              else "+ all-gather of packed tiles)")
                                            if args.mode.startswith("tiles") else
                                            f"view-sharded x{world} (packed triplane+MLP broadcast + "
                                            + ("NVLink peer stores)" if args.mode == "views-p2p"

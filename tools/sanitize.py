@@ -48,6 +48,16 @@ for dtype in ("bf16", "f32"):
         api.dmv3d_render_ddim_step_batched(tb, torch.stack([intr, intr]), torch.stack([c2w, c2w]), H, W,
                                            mlp, ab, 980, 960, xb, samples_per_ray=N, engine="tcgen05",
                                            term_eps=1e-4)
+# interleaved-tile merge: pack two ranks' tiles, unpack (ragged 12x10 image, T = 8)
+nmax = api.tiles_per_rank(4, H, W, 8, 2)
+g3 = torch.zeros((2 * nmax, 3, 8, 8), device="cuda")
+g1 = torch.zeros((2 * nmax, 8, 8), device="cuda")
+gx = torch.zeros((2 * nmax, 3, 8, 8), device="cuda")
+for r in range(2):
+    b = slice(r * nmax, (r + 1) * nmax)
+    api.dmv3d_tiles_pack(intr, c2w, H, W, 8, r, 2, rgb, alpha, xp, g3[b], g1[b], gx[b], 2)
+api.dmv3d_tiles_unpack(intr, c2w, H, W, 8, 2, g3, g1, gx, torch.empty_like(rgb), torch.empty_like(alpha),
+                       torch.empty_like(xp), 2)
 api.dmv3d_plucker_rays(intr, c2w, H, W)
 for rpt in ("1", "2", "4"):  # every store width of the Plucker kernel, with a cut ray range
     os.environ["DMV3D_PLUCKER_RPT"] = rpt
