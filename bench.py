@@ -198,7 +198,7 @@ def main():
                          "triplane broadcast + all-gather per step (strong scaling); views-p2p: "
                          "the same split, outputs assembled by the render kernel's NVLink peer "
                          "stores into symmetric memory; tiles: one asset's 16x16 ray tiles dealt "
-                         "round robin to the ranks, outputs assembled by one all-reduce; tiles-p2p: "
+                         "round robin to the ranks, outputs assembled by one all-gather of packed tiles; tiles-p2p: "
                          "the same, assembled by the render kernel's NVLink peer stores")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
