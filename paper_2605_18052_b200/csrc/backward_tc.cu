@@ -126,7 +126,7 @@ size_t tc_backward_workspace_bytes(int R, int HD) {
 
 bool tc_backward_supported(int C, int HD, int L) {
   return tc_supported(C, HD, L) && bw_smem_bytes<1>(L) <= kSmemLimit &&
-         kHD + (L - 2) * kHD + 16 <= 512;
+         kHD + (L - 2) * kHD + 16 + 48 <= 512;
 }
 
 template <int NG>
@@ -192,13 +192,20 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_after();
   // TMEM per group: the accumulator (z / dh / dG) and the group's own dW^T accumulators
   // (not shared between groups: accumulating into one region would chain the groups' MMAs)
-  const uint32_t tmem = sh->tmem_base + (uint32_t)g * (kHD + ndw);
+  // + 48 columns: the forward pass's fp16 activation operand (32 columns of h_l, the
+  // constant bias K block, padding) -- the forward MMAs read A from TMEM, so the h tiles
+  // written for the backward's MMAs need no proxy fence until the first backward trip
+  const uint32_t gcols = kHD + ndw + 48u;
+  const uint32_t tmem = sh->tmem_base + (uint32_t)g * gcols;
   const uint32_t tmem_dw = tmem + (uint32_t)kHD;
+  const uint32_t tmem_a = tmem + kHD + ndw;  // activation operand (lane = row)
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tmem_row = tmem + lane_off;
   {  // zero this group's dW accumulators (its 4 warps cover the 128 lanes)
     const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     for (uint32_t c = 0; c < ndw; c += 16) ptx::tmem_st16(tmem_dw + lane_off + c, z);
+    const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // k = 64: 1.0
+    ptx::tmem_st8(tmem_a + lane_off + kHD / 2, bias);
     ptx::tmem_st_wait();
   }
   ptx::tc_fence_before();
@@ -416,24 +423,26 @@ __global__ void __launch_bounds__(128 * NG, 1)
           ptx::tmem_ld32(tmem_row + 32 * hh, vv);
           ptx::tmem_ld_wait();
           const float *f = reinterpret_cast<const float *>(vv);
+          uint32_t pk[16];
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            ptx::sts128(hT(l) + hrow + (uint32_t)((4 * hh + c) * 128),
-                        ptx::pack_relu_f16x2(f[8 * c], f[8 * c + 1]),
-                        ptx::pack_relu_f16x2(f[8 * c + 2], f[8 * c + 3]),
-                        ptx::pack_relu_f16x2(f[8 * c + 4], f[8 * c + 5]),
-                        ptx::pack_relu_f16x2(f[8 * c + 6], f[8 * c + 7]));
+          for (int c = 0; c < 16; ++c) pk[c] = ptx::pack_relu_f16x2(f[2 * c], f[2 * c + 1]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)  // the backward's copy (h_l's smem tile)
+            ptx::sts128(hT(l) + hrow + (uint32_t)((4 * hh + c) * 128), pk[4 * c], pk[4 * c + 1],
+                        pk[4 * c + 2], pk[4 * c + 3]);
+          ptx::tmem_st16(tmem_a + lane_off + 16 * hh, pk);  // the forward MMA's A operand
         }
-        sync_for_mma();
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::bar_sync(bar_id, 128);
         if (tid == 0) {
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           const bool head = l == L - 1;
           const int nks = head ? kHD / 16 : (int)kWK / 16;  // the head's bias is added at readout
           for (int ks = 0; ks < nks; ++ks) {
-            const uint64_t ad = ptx::smem_desc(hT(l) + ks * 256, 128, kHSbo, 0);
             const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ss(tmem, ad, bd, head ? id_head : id_hidden, ks > 0 ? 1u : 0u);
+            ptx::mma_f16_ts(tmem, tmem_a + ks * 8, bd, head ? id_head : id_hidden, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&sh->mbar[g]);
         }
@@ -800,7 +809,7 @@ cudaError_t launch_render_backward_tc(const RenderParams &P0, const GradParams &
   const int nv = (int)((P.ray_end - 1) / HW - P.ray_begin / HW + 1);
   const int64_t npatch = (int64_t)nv * ((P.H + 3) / 4) * ((P.W + 3) / 4);
   timer_begin(P.timer, st);
-  const bool ng2 = bw_smem_bytes<2>(P.L) <= kSmemLimit && 2 * (kHD + (P.L - 2) * kHD + 16) <= 512;
+  const bool ng2 = bw_smem_bytes<2>(P.L) <= kSmemLimit && 2 * (kHD + (P.L - 2) * kHD + 16 + 48) <= 512;
   e = ng2 ? launch_bwd_k1<2>(P, Gp, dG, sms, npatch, st) : launch_bwd_k1<1>(P, Gp, dG, sms, npatch, st);
   timer_end(P.timer, st);
   if (e != cudaSuccess) return e;
