@@ -72,6 +72,7 @@ constexpr size_t kSmemLimit = 232448;
 template <int NG>
 struct BwShared {
   uint64_t mbar[NG];
+  uint64_t mbar2[NG];  // the weight-gradient chain, issued by a second thread of the group
   uint32_t tmem_base;
   int patch[NG];
   int bbox[NG][2][8];
@@ -154,7 +155,10 @@ __global__ void __launch_bounds__(128 * NG, 1)
 
   // ---- prologue: barriers, TMEM, weights, the constant [1, 0...] columns of the h tiles
   if (tid_cta == 0) {
-    for (int i = 0; i < NG; ++i) ptx::mbar_init(&sh->mbar[i], 1);
+    for (int i = 0; i < NG; ++i) {
+      ptx::mbar_init(&sh->mbar[i], 1);
+      ptx::mbar_init(&sh->mbar2[i], 1);
+    }
     for (int i = 0; i < NG; ++i)
       for (int p = 0; p < 2; ++p)
         for (int e = 0; e < 8; ++e) sh->bbox[i][p][e] = (e < 4) ? 0x7fffffff : -1;
@@ -242,6 +246,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
   auto mma_wait = [&]() {
     ptx::mbar_wait(&sh->mbar[g], mphase);
     mphase ^= 1u;
+    ptx::tc_fence_after();
+  };
+  // backward trips: the dh chain (thread 0, mbar) and the dW chain (thread 32, mbar2) are
+  // issued by two threads, so their instruction issue overlaps
+  uint32_t mphase2 = 0;
+  auto mma_wait2 = [&]() {
+    ptx::mbar_wait(&sh->mbar[g], mphase);
+    mphase ^= 1u;
+    ptx::mbar_wait(&sh->mbar2[g], mphase2);
+    mphase2 ^= 1u;
     ptx::tc_fence_after();
   };
   // all rows' smem / TMEM accesses done -> the elected thread may issue
@@ -559,13 +573,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
         const uint32_t whead = sW + (uint32_t)((L - 2) * kWHidden);
         ptx::mma_f16_ss(tmem, ptx::smem_desc(sB, 128, kDoSbo, 0), ptx::smem_desc(whead, kWSbo, 128, 0),
                         id_dh, 0u);
+        ptx::mma_commit(&sh->mbar[g]);
+      } else if (tid == 32) {
+        ptx::tc_fence_after();
         const uint32_t dcol = tmem_dw + (uint32_t)((L - 2) * kHD);
         for (int ks = 0; ks < 8; ++ks)
           ptx::mma_f16_ss(dcol, ptx::smem_desc(hT(L - 1) + ks * 2 * kHSbo, kHSbo, 128, 0),
                           ptx::smem_desc(sB + ks * 2 * kDoSbo, kDoSbo, 128, 0), id_dw_head, 1u);
-        ptx::mma_commit(&sh->mbar[g]);
+        ptx::mma_commit(&sh->mbar2[g]);
       }
-      mma_wait();
+      mma_wait2();
       // ---- hidden layers l = L-2 .. 0: dz_l = dh_{l+1} (.) [h_{l+1} > 0] over h_{l+1}'s tile
       for (int l = L - 2; l >= 0; --l) {
         const uint32_t ht = hT(l + 1);
@@ -585,24 +602,25 @@ __global__ void __launch_bounds__(128 * NG, 1)
         }
         sync_for_mma();
         if (l == 0) break;
+        // dh_l = dz_l W_l: A = dz_l (K-major, K = 64 outputs), B = W_l as [out][in] MN-major
+        // (thread 0); [h_l | 1]^T dz_l -> dW_l^T (rows 0..63), db_l (row 64), K = the 128
+        // samples (thread 32): two issuing threads, two mbarriers
         if (tid == 0) {
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
-          // dh_l = dz_l W_l: A = dz_l (K-major, K = 64 outputs), B = W_l as [out][in] MN-major;
-          // [h_l | 1]^T dz_l -> dW_l^T (rows 0..63), db_l (row 64), K = the 128 samples.
-          // The two accumulation chains are issued interleaved: the tensor pipe overlaps
-          // independent chains but runs one chain's dependent K-steps back to back.
+          for (int ks = 0; ks < kHD / 16; ++ks)
+            ptx::mma_f16_ss(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
+                            ptx::smem_desc(wbase + ks * 2 * kWSbo, kWSbo, 128, 0), id_dh, ks > 0 ? 1u : 0u);
+          ptx::mma_commit(&sh->mbar[g]);
+        } else if (tid == 32) {
+          ptx::tc_fence_after();
           const uint32_t dcol = tmem_dw + (uint32_t)((l - 1) * kHD);
-          for (int ks = 0; ks < 8; ++ks) {
-            if (ks < kHD / 16)
-              ptx::mma_f16_ss(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
-                              ptx::smem_desc(wbase + ks * 2 * kWSbo, kWSbo, 128, 0), id_dh, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < 8; ++ks)
             ptx::mma_f16_ss(dcol, ptx::smem_desc(hT(l) + ks * 2 * kHSbo, kHSbo, 128, 0),
                             ptx::smem_desc(ht + ks * 2 * kHSbo, kHSbo, 128, 0), id_dw, 1u);
-          }
-          ptx::mma_commit(&sh->mbar[g]);
+          ptx::mma_commit(&sh->mbar2[g]);
         }
-        mma_wait();
+        mma_wait2();
       }
       // ---- dG_window = A_blend^T dz0 (dz0 is in h_1's tile), one pass per window
       const int nwin = (ktot + kKW - 1) / kKW;
