@@ -96,10 +96,12 @@ struct TcShared {
   unsigned n_tiles[NG], n_kcols[NG];  // blend windows issued, staged K columns (counters[4..5])
 };
 
+// dynamic shared memory of the render kernel (tiles + weights); the TcShared block is a
+// static __shared__ variable (so its accesses compile to LDS/STS/ATOMS, not generic ones)
 template <int NG>
 static size_t tc_smem_bytes(int L) {
   return 1024 /*align slack*/ + (size_t)NG * (kATileBytes + kBTileBytes) +
-         (size_t)(L - 2) * kWHidden + kWHead + sizeof(TcShared<NG>);
+         (size_t)(L - 2) * kWHidden + kWHead;
 }
 
 // ------------------------------------------------------------------ K0
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
   uint8_t *tileB0 = smem + NG * kATileBytes;
   uint8_t *wsm = tileB0 + NG * kBTileBytes;
   const int L = P.L;
-  TcShared<NG> *sh = reinterpret_cast<TcShared<NG> *>(wsm + (L - 2) * kWHidden + kWHead);
+  __shared__ TcShared<NG> sh_s;
+  TcShared<NG> *sh = &sh_s;
 
   const int tid_cta = threadIdx.x;
   const int g = tid_cta >> 7;     // group
@@ -571,16 +574,18 @@ __global__ void __launch_bounds__(128 * NG, 1)
         ptx::cp_async_wait_all();
         ptx::fence_proxy_async_smem();
         ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
+        if (tid < 32) {  // the group's warp 0 issues (one elected lane, warp-uniform code)
           ptx::tc_fence_after();
           for (int ks = 0; ks < kpad / 16; ++ks) {
             const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
             const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-            ptx::mma_f16_ss(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_f16_ss_warp(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&sh->mbar[g]);
-          sh->n_tiles[g] += 1u;  // issuing thread only: plain shared-memory counters
-          sh->n_kcols[g] += (unsigned)kpad;
+          ptx::mma_commit_warp(&sh->mbar[g]);
+          if (tid == 0) {  // plain shared-memory counters
+            sh->n_tiles[g] += 1u;
+            sh->n_kcols[g] += (unsigned)kpad;
+          }
         }
         ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         PH(4);
         ptx::tc_fence_before();
         ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
+        if (tid < 32) {
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
@@ -616,16 +621,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
               for (int hx = 0; hx < 2; ++hx) {
                 const int kk = 2 * hx + ks;
                 const uint64_t bd = ptx::smem_desc(wbase + kk * 256, 128, kWSbo, 0);
-                ptx::mma_f16_ts(tmem + (hx ? kHeadAlt : 0u), tmem + kTcHD + kk * 8, bd, id, ks > 0 ? 1u : 0u);
+                ptx::mma_f16_ts_warp(tmem + (hx ? kHeadAlt : 0u), tmem + kTcHD + kk * 8, bd, id, ks > 0 ? 1u : 0u);
               }
           } else {
 #pragma unroll
             for (int ks = 0; ks < (int)kWK / 16; ++ks) {
               const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-              ptx::mma_f16_ts(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
+              ptx::mma_f16_ts_warp(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
             }
           }
-          ptx::mma_commit(&sh->mbar[g]);
+          ptx::mma_commit_warp(&sh->mbar[g]);
         }
         ptx::mbar_wait(&sh->mbar[g], mphase);
         mphase ^= 1u;
@@ -832,7 +837,7 @@ cudaError_t launch_render_tc(const RenderParams &P0, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   // K1: persistent render, one CTA per SM; as many groups as shared memory allows
   P.tp = ws;  // the render kernel reads the workspace (counter + G)
-  const bool ng4 = tc_smem_bytes<4>(P.L) <= kSmemLimit;
+  const bool ng4 = tc_smem_bytes<4>(P.L) + sizeof(TcShared<4>) <= kSmemLimit;
   timer_begin(P.timer, st);
   if (grid_mode) {
     const int Gr = P.grid_res;
