@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int bar_id = 1 + g;
   uint8_t *gbase = smem + (size_t)g * group_bytes(L);
   uint8_t *wsm = smem + (size_t)NG * group_bytes(L);
-  BwShared<NG> *sh = reinterpret_cast<BwShared<NG> *>(wsm + (L - 2) * kWHidden + kWHead);
+  __shared__ BwShared<NG> sh_s;  // static: LDS/STS/ATOMS rather than generic accesses
+  BwShared<NG> *sh = &sh_s;
 
   const uint32_t sB = ptx::smem_u32(gbase);             // staged texels, then d_o
   const uint32_t sA = sB + kBBytes;                      // sparse blend A
@@ -414,14 +415,14 @@ __global__ void __launch_bounds__(128 * NG, 1)
         scatter_a(w0);
         ptx::cp_async_wait_all();
         sync_for_mma();
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0 issues (elected lane)
           ptx::tc_fence_after();
           for (int ks = 0; ks < kpad / 16; ++ks) {
             const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
             const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-            ptx::mma_f16_ss(tmem, ad, bd, id_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_f16_ss_warp(tmem, ad, bd, id_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&sh->mbar[g]);
+          ptx::mma_commit_warp(&sh->mbar[g]);
         }
         mma_wait();
       }
@@ -449,16 +450,16 @@ __global__ void __launch_bounds__(128 * NG, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::bar_sync(bar_id, 128);
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0 issues (elected lane)
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           const bool head = l == L - 1;
           const int nks = head ? kHD / 16 : (int)kWK / 16;  // the head's bias is added at readout
           for (int ks = 0; ks < nks; ++ks) {
             const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
-            ptx::mma_f16_ts(tmem, tmem_a + ks * 8, bd, head ? id_head : id_hidden, ks > 0 ? 1u : 0u);
+            ptx::mma_f16_ts_warp(tmem, tmem_a + ks * 8, bd, head ? id_head : id_hidden, ks > 0 ? 1u : 0u);
           }
-          ptx::mma_commit(&sh->mbar[g]);
+          ptx::mma_commit_warp(&sh->mbar[g]);
         }
         mma_wait();
       }
@@ -568,19 +569,19 @@ __global__ void __launch_bounds__(128 * NG, 1)
       ptx::sts128(dorow + 128, 0u, 0u, 0u, 0u);
       sync_for_mma();
       // ---- head: dh_{L-1} = d_o W_{L-1}; [h_{L-1} | 1]^T d_o -> dW_{L-1}^T, db_{L-1}
-      if (tid == 0) {
+      if (tid < 32) {  // warp 0 issues (elected lane)
         ptx::tc_fence_after();
         const uint32_t whead = sW + (uint32_t)((L - 2) * kWHidden);
-        ptx::mma_f16_ss(tmem, ptx::smem_desc(sB, 128, kDoSbo, 0), ptx::smem_desc(whead, kWSbo, 128, 0),
+        ptx::mma_f16_ss_warp(tmem, ptx::smem_desc(sB, 128, kDoSbo, 0), ptx::smem_desc(whead, kWSbo, 128, 0),
                         id_dh, 0u);
-        ptx::mma_commit(&sh->mbar[g]);
-      } else if (tid == 32) {
+        ptx::mma_commit_warp(&sh->mbar[g]);
+      } else if (tid < 64) {  // warp 1 issues the dW chain
         ptx::tc_fence_after();
         const uint32_t dcol = tmem_dw + (uint32_t)((L - 2) * kHD);
         for (int ks = 0; ks < 8; ++ks)
-          ptx::mma_f16_ss(dcol, ptx::smem_desc(hT(L - 1) + ks * 2 * kHSbo, kHSbo, 128, 0),
+          ptx::mma_f16_ss_warp(dcol, ptx::smem_desc(hT(L - 1) + ks * 2 * kHSbo, kHSbo, 128, 0),
                           ptx::smem_desc(sB + ks * 2 * kDoSbo, kDoSbo, 128, 0), id_dw_head, 1u);
-        ptx::mma_commit(&sh->mbar2[g]);
+        ptx::mma_commit_warp(&sh->mbar2[g]);
       }
       mma_wait2();
       // ---- hidden layers l = L-2 .. 0: dz_l = dh_{l+1} (.) [h_{l+1} > 0] over h_{l+1}'s tile
@@ -605,20 +606,20 @@ __global__ void __launch_bounds__(128 * NG, 1)
         // dh_l = dz_l W_l: A = dz_l (K-major, K = 64 outputs), B = W_l as [out][in] MN-major
         // (thread 0); [h_l | 1]^T dz_l -> dW_l^T (rows 0..63), db_l (row 64), K = the 128
         // samples (thread 32): two issuing threads, two mbarriers
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0 issues (elected lane)
           ptx::tc_fence_after();
           const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
           for (int ks = 0; ks < kHD / 16; ++ks)
-            ptx::mma_f16_ss(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
+            ptx::mma_f16_ss_warp(tmem, ptx::smem_desc(ht + ks * 256, 128, kHSbo, 0),
                             ptx::smem_desc(wbase + ks * 2 * kWSbo, kWSbo, 128, 0), id_dh, ks > 0 ? 1u : 0u);
-          ptx::mma_commit(&sh->mbar[g]);
-        } else if (tid == 32) {
+          ptx::mma_commit_warp(&sh->mbar[g]);
+        } else if (tid < 64) {  // warp 1 issues the dW chain
           ptx::tc_fence_after();
           const uint32_t dcol = tmem_dw + (uint32_t)((l - 1) * kHD);
           for (int ks = 0; ks < 8; ++ks)
-            ptx::mma_f16_ss(dcol, ptx::smem_desc(hT(l) + ks * 2 * kHSbo, kHSbo, 128, 0),
+            ptx::mma_f16_ss_warp(dcol, ptx::smem_desc(hT(l) + ks * 2 * kHSbo, kHSbo, 128, 0),
                             ptx::smem_desc(ht + ks * 2 * kHSbo, kHSbo, 128, 0), id_dw, 1u);
-          ptx::mma_commit(&sh->mbar2[g]);
+          ptx::mma_commit_warp(&sh->mbar2[g]);
         }
         mma_wait2();
       }
@@ -632,12 +633,12 @@ __global__ void __launch_bounds__(128 * NG, 1)
           scatter_a(w0);
           sync_for_mma();
         }
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0 issues (elected lane)
           ptx::tc_fence_after();
           for (int ks = 0; ks < 8; ++ks)
-            ptx::mma_f16_ss(tmem, ptx::smem_desc(sA + ks * 2 * kASbo, kASbo, 128, 0),
+            ptx::mma_f16_ss_warp(tmem, ptx::smem_desc(sA + ks * 2 * kASbo, kASbo, 128, 0),
                             ptx::smem_desc(hT(1) + ks * 2 * kHSbo, kHSbo, 128, 0), id_dg, ks > 0 ? 1u : 0u);
-          ptx::mma_commit(&sh->mbar[g]);
+          ptx::mma_commit_warp(&sh->mbar[g]);
         }
         mma_wait();
         ptx::bar_sync(bar_id, 128);  // the table is complete (nwin == 1: written in forward)
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(288)
 template <int NG>
 static cudaError_t launch_bwd_k1(const RenderParams &P, const GradParams &Gp, float *dG, int sms,
                                  int64_t npatch, cudaStream_t st) {
-  const size_t s1 = bw_smem_bytes<NG>(P.L);
+  const size_t s1 = bw_smem_bytes<NG>(P.L) - sizeof(BwShared<NG>);  // dynamic part
   cudaError_t e = cudaFuncSetAttribute(render_bwd_tc_kernel<NG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
   if (e != cudaSuccess) return e;
