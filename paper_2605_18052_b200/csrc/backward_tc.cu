@@ -139,9 +139,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
                                               ~uintptr_t(1023));
   const int L = P.L;
   const int tid_cta = threadIdx.x;
-  const int g = tid_cta >> 7;
+  const int warp = __shfl_sync(0xffffffffu, tid_cta >> 5, 0);  // warp-uniform (see render_tc)
+  const int g = warp >> 2;
   const int tid = tid_cta & 127;
-  const int warp = tid_cta >> 5;
   const int bar_id = 1 + g;
   uint8_t *gbase = smem + (size_t)g * group_bytes(L);
   uint8_t *wsm = smem + (size_t)NG * group_bytes(L);

@@ -260,9 +260,12 @@ __global__ void __launch_bounds__(128 * NG, 1)
   TcShared<NG> *sh = &sh_s;
 
   const int tid_cta = threadIdx.x;
-  const int g = tid_cta >> 7;     // group
+  // warp index through a shuffle: ptxas then knows it (and the group, the group's TMEM
+  // columns, tile addresses and MMA descriptors derived from it) is warp-uniform and keeps
+  // them in uniform registers -- no R2UR per MMA issue
+  const int warp = __shfl_sync(0xffffffffu, tid_cta >> 5, 0);
+  const int g = warp >> 2;        // group
   const int tid = tid_cta & 127;  // row within the group's tile
-  const int warp = tid_cta >> 5;
   const int bar_id = 1 + g;
 
   // ---- prologue: barriers, TMEM, weights (fp16, K-major, bias column)
