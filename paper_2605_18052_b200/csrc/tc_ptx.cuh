@@ -39,7 +39,7 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#ifdef DMV3D_MBAR_NOHINT
+#ifndef DMV3D_MBAR_HINT  // plain try_wait (A/B: -0.15 % on the cfg3 step vs a 1 ms suspend hint)
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
