@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = sh->tmem_base + (uint32_t)(g * 2 * kTcHD);
+  // TMEM base through a shuffle: warp-uniform (uniform registers in the MMA issue)
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sh->tmem_base, 0) + (uint32_t)(g * 2 * kTcHD);
   const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   {  // the activation operand's bias K block ([1, 0 x 15] per row) is constant: once
     const uint32_t bias[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -312,9 +313,20 @@ __global__ void __launch_bounds__(128 * NG, 1)
     ptx::tmem_st_wait();
   }
 
-  const uint32_t sA = ptx::smem_u32(tileA0 + g * kATileBytes);
-  const uint32_t sB = ptx::smem_u32(tileB0 + g * kBTileBytes);
-  const uint32_t sW = ptx::smem_u32(wsm);
+  // tile addresses from a warp-uniform (shuffled) 32-bit base: ptxas keeps them and the
+  // descriptor words built from them in uniform registers
+  const uint32_t sbase = __shfl_sync(0xffffffffu, ptx::smem_u32(tileA0), 0);
+  const uint32_t sA = sbase + (uint32_t)(g * kATileBytes);
+  const uint32_t sB = sbase + (uint32_t)(NG * kATileBytes + g * kBTileBytes);
+  const uint32_t sW = sbase + (uint32_t)(NG * (kATileBytes + kBTileBytes));
+  // low descriptor words of each operand's first K step (start address >> 4 | LBO >> 4
+  // << 16); a K step adds its byte offset >> 4 (no carry out of the 14-bit field)
+  const uint32_t a_lo0 = ((sA >> 4) & 0x3FFFu) | ((128u >> 4) << 16);
+  const uint32_t b_lo0 = ((sB >> 4) & 0x3FFFu) | ((1024u >> 4) << 16);
+  const uint32_t w_lo0 = ((sW >> 4) & 0x3FFFu) | ((128u >> 4) << 16);
+  constexpr uint64_t a_hi = ((uint64_t)(kASbo >> 4) << 32) | (1ull << 46);
+  constexpr uint64_t b_hi = ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
+  constexpr uint64_t w_hi = ((uint64_t)(kWSbo >> 4) << 32) | (1ull << 46);
   const uint32_t sArow = sA + a_row(tid);
   constexpr uint32_t idesc_blend = ptx::idesc_f16(128, kTcHD, 1);
   constexpr uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
@@ -580,9 +592,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
         if (tid < 32) {  // the group's warp 0 issues (one elected lane, warp-uniform code)
           ptx::tc_fence_after();
           for (int ks = 0; ks < kpad / 16; ++ks) {
-            const uint64_t ad = ptx::smem_desc(sA + ks * 256, 128, kASbo, 0);
-            const uint64_t bd = ptx::smem_desc(sB + ks * 2048, 1024, 1024, 2);
-            ptx::mma_f16_ss_warp(tmem, ad, bd, idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_f16_ss_warp(tmem, a_hi | (a_lo0 + (uint32_t)(ks * 16)), b_hi | (b_lo0 + (uint32_t)(ks * 128)),
+                                 idesc_blend, (w0 > 0 || ks > 0) ? 1u : 0u);
           }
           ptx::mma_commit_warp(&sh->mbar[g]);
           if (tid == 0) {  // plain shared-memory counters
@@ -612,7 +623,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
         ptx::bar_sync(bar_id, 128);
         if (tid < 32) {
           ptx::tc_fence_after();
-          const uint32_t wbase = sW + (uint32_t)((l - 1) * kWHidden);
+          const uint32_t wlo = w_lo0 + (uint32_t)((l - 1) * (kWHidden >> 4));
           const uint32_t id = (l == L - 1) ? idesc_head : idesc_hidden;
           // the head skips its bias K block (4 FADDs at readout instead of an MMA)
           if (l == L - 1) {
@@ -623,13 +634,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
 #pragma unroll
               for (int hx = 0; hx < 2; ++hx) {
                 const int kk = 2 * hx + ks;
-                const uint64_t bd = ptx::smem_desc(wbase + kk * 256, 128, kWSbo, 0);
+                const uint64_t bd = w_hi | (wlo + (uint32_t)(kk * 16));
                 ptx::mma_f16_ts_warp(tmem + (hx ? kHeadAlt : 0u), tmem + kTcHD + kk * 8, bd, id, ks > 0 ? 1u : 0u);
               }
           } else {
 #pragma unroll
             for (int ks = 0; ks < (int)kWK / 16; ++ks) {
-              const uint64_t bd = ptx::smem_desc(wbase + ks * 256, 128, kWSbo, 0);
+              const uint64_t bd = w_hi | (wlo + (uint32_t)(ks * 16));
               ptx::mma_f16_ts_warp(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
             }
           }
