@@ -331,7 +331,6 @@ __global__ void __launch_bounds__(128 * NG, 1)
   constexpr uint32_t idesc_blend = ptx::idesc_f16(128, kTcHD, 1);
   constexpr uint32_t idesc_hidden = ptx::idesc_f16(128, kTcHD, 0);
   constexpr uint32_t idesc_head = ptx::idesc_f16(128, 16, 0);
-  constexpr uint32_t idesc_hidden32 = ptx::idesc_f16(128, 32, 0);
 
   const __half *G0 = reinterpret_cast<const __half *>(reinterpret_cast<const uint8_t *>(P.tp) +
                                                        kWsHeader);
@@ -643,25 +642,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
                 ptx::mma_f16_ts_warp(tmem + (hx ? kHeadAlt : 0u), tmem + kTcHD + kk * 8, bd, id, ks > 0 ? 1u : 0u);
               }
           } else {
-#ifdef DMV3D_NSPLIT
-            // hidden layer as two independent N = 32 chains (output columns 0-31 and
-            // 32-63), their K steps interleaved: each step's accumulation dependency is
-            // separated by an independent MMA in the tensor pipe's queue
-#pragma unroll
-            for (int ks = 0; ks < (int)kWK / 16; ++ks)
-#pragma unroll
-              for (int nh = 0; nh < 2; ++nh) {
-                const uint64_t bd = w_hi | (wlo + (uint32_t)(ks * 16 + nh * 4 * (kWSbo >> 4)));
-                ptx::mma_f16_ts_warp(tmem + (uint32_t)(nh * 32), tmem + kTcHD + ks * 8, bd, idesc_hidden32,
-                                     ks > 0 ? 1u : 0u);
-              }
-#else
 #pragma unroll
             for (int ks = 0; ks < (int)kWK / 16; ++ks) {
               const uint64_t bd = w_hi | (wlo + (uint32_t)(ks * 16));
               ptx::mma_f16_ts_warp(tmem, tmem + kTcHD + ks * 8, bd, id, ks > 0 ? 1u : 0u);
             }
-#endif
           }
           ptx::mma_commit_warp(&sh->mbar[g]);
         }
