@@ -65,8 +65,10 @@ constexpr uint32_t kHeadAlt = 112;  // second head accumulator: spare TMEM colum
 constexpr uint32_t kWsHeader = kTcWsHeader;
 
 // shared-memory carve-up (bytes)
-constexpr uint32_t kATileBytes = 128 * kTcKMax * 2;    // 32 KiB, K-major, SBO 2048
-constexpr uint32_t kASbo = (kTcKMax / 8) * 128;        // 2048
+// sparse A tile, K-major SWIZZLE_NONE: 8-row groups SBO = 2048 + 32 bytes apart, so rows
+// m, m+8, m+16, m+24 of a warp fall into different banks (the 2-byte weight scatter)
+constexpr uint32_t kASbo = (kTcKMax / 8) * 128 + 32;   // 2080
+constexpr uint32_t kATileBytes = 16 * kASbo;           // 32.5 KiB (NG of them keep 1 KiB alignment)
 constexpr uint32_t kBTileBytes = kTcKMax * kTcHD * 2;  // 16 KiB, 128 B per texel row
 constexpr uint32_t kWK = kTcHD + 16;                   // weights K incl. bias column
 constexpr uint32_t kWSbo = (kWK / 8) * 128;            // 1280
