@@ -385,8 +385,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
     const int ktex = base2 + ext1 * ext2;
     const int ktot = ktex + hb;
     const int kpad = (min(kTcKMax, ktot - w0) + 15) & ~15;
-    if (tid < kpad) {
-      const int kg = w0 + tid;
+    // column col = tid + 64 (mod 128): a window of <= 64 columns is staged by warps 2-3,
+    // keeping warp 0 (the MMA issuer, the group's critical warp) and warp 1 free
+    const int col = (tid + 64) & 127;
+    if (col < kpad) {
+      const int kg = w0 + col;
       int texel = -1;
       if (kg == ktex && hb) {
         texel = 3 * R * R;
@@ -400,14 +403,14 @@ __global__ void __launch_bounds__(128 * NG, 1)
         const int rr = (int)(((float)loc + 0.5f) * __fdividef(1.0f, (float)bw));
         texel = (pl * R + tb0 + rr) * R + ta0 + (loc - rr * bw);
       }
-      sh->coltex[g][tid] = texel;
-      if (direct) {  // this thread stages texel row tid itself: no table round trip
-        const uint32_t drow = sB + (uint32_t)(tid << 7);
+      sh->coltex[g][col] = texel;
+      if (direct) {  // this thread stages texel row col itself: no table round trip
+        const uint32_t drow = sB + (uint32_t)(col << 7);
         const __half *src = G + (size_t)max(texel, 0) * kTcHD;
         const uint32_t nb = texel >= 0 ? 16u : 0u;
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch)
-          ptx::cp_async16(drow + (uint32_t)((ch ^ (tid & 7)) << 4), src + ch * 8, nb);
+          ptx::cp_async16(drow + (uint32_t)((ch ^ (col & 7)) << 4), src + ch * 8, nb);
       }
     }
   };
