@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
   };
 
   while (true) {
-    if (tid == 0) sh->patch[g] = (int)atomicAdd(counter, 1u);
+    if (tid == 127) sh->patch[g] = (int)atomicAdd(counter, 1u);  // warp 3: off the issuer
     ptx::bar_sync(bar_id, 128);
     const int64_t patch = sh->patch[g];
     if (patch >= npatch) break;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(128 * NG, 1)
       }
       ptx::bar_sync(bar_id, 128);
       // reset the other parity's slot for the next chunk (all its readers passed a barrier)
-      if (tid < 8) sh->bbox[g][par ^ 1][tid] = (tid < 4) ? 0x7fffffff : -1;
+      if (tid >= 120) sh->bbox[g][par ^ 1][tid - 120] = (tid < 124) ? 0x7fffffff : -1;  // warp 3
       fill_table(sh->bbox[g][par], 0, true);
     };
 
