@@ -14,3 +14,5 @@ timeout 600 python bench.py --config cfg2 --no-cpu-baseline --sustained-s 0 > $O
 timeout 900 python tools/sweep.py > $O/sweep.jsonl 2> $O/sweep.err
 bash tools/gpu_variants.sh > /dev/null 2>&1
 echo done-main
+# phase split of the render kernel (DMV3D_PHASES build, prebuilt in-tree)
+[ -f paper_2605_18052_b200/libdmv3d_phases.so ] && DMV3D_LIB=$PWD/paper_2605_18052_b200/libdmv3d_phases.so timeout 300 python tools/phases.py > $O/phases.txt 2>&1
