@@ -102,6 +102,8 @@ struct TcShared {
 // static __shared__ variable (so its accesses compile to LDS/STS/ATOMS, not generic ones)
 template <int NG>
 static size_t tc_smem_bytes(int L) {
+  // the B tiles follow the NG A tiles and must stay 1 KiB aligned (SWIZZLE_128B atoms)
+  static_assert((NG * kATileBytes) % 1024 == 0, "A tiles must keep the B tiles 1 KiB aligned");
   return 1024 /*align slack*/ + (size_t)NG * (kATileBytes + kBTileBytes) +
          (size_t)(L - 2) * kWHidden + kWHead;
 }
