@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(256)
 __device__ __forceinline__ uint32_t a_row(int m) {
   return (uint32_t)((m >> 3) * kASbo + (m & 7) * 16);
 }
-__device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(((k >> 3) << 7) | ((k & 7) << 1)); }
+// byte offset of column k in a row: (k >> 3) * 128 + (k & 7) * 2 == 2 k + 112 (k >> 3)
+// (k >= 0): a shift and two multiply-adds instead of shift / mask / or chains
+__device__ __forceinline__ uint32_t a_col(int k) { return (uint32_t)(2 * k + 112 * (k >> 3)); }
 
 // hidden activation (reading A5) -> fp16 pair; ReLU folds into the conversion, SiLU and
 // softplus are evaluated in fp32 (fast-math exp / log, within the tensor-core tolerance)
