@@ -399,11 +399,11 @@ __global__ void __launch_bounds__(128 * NG, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           if (one_window || (unsigned)cs[e] < (unsigned)kp)  // one window holds every column
-            ptx::sts16(sArow + (uint32_t)(((cs[e] >> 3) << 7) | ((cs[e] & 7) << 1)),
+            ptx::sts16(sArow + (uint32_t)(2 * cs[e] + 112 * (cs[e] >> 3)),  // (c>>3)*128 + (c&7)*2
                        ptx::f32_to_f16(w4[e]));
       }
       if (hb && (unsigned)(ktex - w0) < (unsigned)kp)
-        ptx::sts16(sArow + (uint32_t)((((ktex - w0) >> 3) << 7) | (((ktex - w0) & 7) << 1)),
+        ptx::sts16(sArow + (uint32_t)(2 * (ktex - w0) + 112 * ((ktex - w0) >> 3)),
                    (uint16_t)0x3c00u);
     };
 
