@@ -369,6 +369,9 @@ __global__ void __launch_bounds__(128 * NG, 1)
   // plane, so b0 is not folded into G but added by one extra A column (weight 1)
   // that reads the bias row G[3 R R]
   const int hb = P.smode != 0 ? 1 : 0;
+  // geometry fast path (uniform): align-corners sampling with power-of-two box extents
+  const bool fastgeo = P.smode == 0 && P.inv_ext[0] != 0.0f && P.inv_ext[1] != 0.0f && P.inv_ext[2] != 0.0f;
+  const float rm1 = __int2float_rn(R - 1);
 
   uint32_t mphase = 0;
   unsigned n_hit = 0, n_samples = 0, n_term = 0, n_rays = 0;  // per thread: fits 32 bits
@@ -526,9 +529,23 @@ __global__ void __launch_bounds__(128 * NG, 1)
           const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
           sample_p(ray, sample_t(ray, delta, k, u), p);
         }
+        if (fastgeo) {  // align-corners mode, power-of-two box extents: texel_coord's
+                        // multiply path with no per-axis branches (the same IEEE ops)
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-          texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
+          for (int a = 0; a < 3; ++a) {
+            const float sx = __fmul_rn(__fsub_rn(p[a], P.lo[a]), P.inv_ext[a]);
+            const float px = fminf(fmaxf(__fmul_rn(sx, rm1), 0.0f), rm1);
+            const int i0 = min(__float2int_rd(px), R - 2);
+            const float f = __fsub_rn(px, __int2float_rn(i0));
+            ix[a] = i0;
+            wl[a] = 1.0f - f;
+            wh[a] = f;
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
+        }
       }
       int mn[3], mx[3];
 #pragma unroll
