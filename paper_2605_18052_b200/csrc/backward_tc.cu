@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
   const int R = P.R;
   const float wscale = (P.agg == 0) ? (1.0f / 3.0f) : 1.0f;
   const int hb = P.smode != 0 ? 1 : 0;
+  const bool fastgeo = P.smode == 0 && P.inv_ext[0] != 0.0f && P.inv_ext[1] != 0.0f && P.inv_ext[2] != 0.0f;
+  const float rm1 = __int2float_rn(R - 1);
   const uint32_t sArow = sA + (uint32_t)((tid >> 3) * kASbo + (tid & 7) * 16);
   const uint32_t hrow = (uint32_t)((tid >> 3) * kHSbo + (tid & 7) * 16);
   const uint32_t dorow = sB + (uint32_t)((tid >> 3) * kDoSbo + (tid & 7) * 16);
@@ -314,9 +316,23 @@ __global__ void __launch_bounds__(128 * NG, 1)
         float p[3];
         const float u = P.jitter ? jitter_u(P.seed, (uint64_t)r * P.N + k) : 0.5f;
         sample_p(ray, sample_t(ray, delta, k, u), p);
+        if (fastgeo) {  // align-corners, power-of-two extents: texel_coord's multiply path
+                        // inline, no per-axis branches (same IEEE ops; see render_tc)
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-          texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
+          for (int a = 0; a < 3; ++a) {
+            const float sx = __fmul_rn(__fsub_rn(p[a], P.lo[a]), P.inv_ext[a]);
+            const float px = fminf(fmaxf(__fmul_rn(sx, rm1), 0.0f), rm1);
+            const int i0 = min(__float2int_rd(px), R - 2);
+            const float f = __fsub_rn(px, __int2float_rn(i0));
+            ix[a] = i0;
+            wl[a] = 1.0f - f;
+            wh[a] = f;
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            texel_axis(p[a], P.lo[a], P.hi[a], P.inv_ext[a], R, P.smode, ix[a], wl[a], wh[a]);
+        }
       }
       int mn[3], mx[3];
 #pragma unroll
