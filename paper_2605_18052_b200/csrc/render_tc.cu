@@ -591,7 +591,14 @@ __global__ void __launch_bounds__(128 * NG, 1)
       for (int w0 = 0; w0 < ktot; w0 += kTcKMax) {
         const int kp = min(kTcKMax, ktot - w0);
         const int kpad = (kp + 15) & ~15;
-        for (int kc = 0; kc < kpad / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
+        // zero the row's kpad columns: kpad / 16 iterations of two 16-B stores (a plain loop;
+        // the compiler's multi-level unrolling of a one-store loop cost ~35 control
+        // instructions per chunk)
+#pragma unroll 1
+        for (int kc = 0; kc < kpad / 16; ++kc) {
+          ptx::sts128(sArow + (uint32_t)(kc << 8), 0u, 0u, 0u, 0u);
+          ptx::sts128(sArow + (uint32_t)((kc << 8) + 128), 0u, 0u, 0u, 0u);
+        }
         if (sv) {
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) {
