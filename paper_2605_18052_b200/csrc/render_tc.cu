@@ -512,9 +512,8 @@ __global__ void __launch_bounds__(128 * NG, 1)
       const int k = kk + q;
       // GRID: one point per row, z advancing 4 per chunk
       const bool sv = spec_alive && (GRID ? gz0 + (kk / kChunk) * 4 < P.grid_res : k < P.N);
-      ix[0] = ix[1] = ix[2] = 0;
-      wl[0] = wl[1] = wl[2] = 0.f;
-      wh[0] = wh[1] = wh[2] = 0.f;
+      // rows without a sample keep the previous chunk's values: nothing reads them (the box
+      // reduction masks them, the scatter skips them: a row live at the scatter was live here)
       if (sv) {
         float p[3];
         if constexpr (GRID) {
