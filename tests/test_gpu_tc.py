@@ -93,6 +93,22 @@ def test_tc_render_jitter():
     assert er < RGB_TOL and ea < ALPHA_TOL
 
 
+@pytest.mark.parametrize("lo,hi", [((-0.6, -0.8, -0.7), (0.9, 0.5, 0.75)),   # extents not 2^k
+                                   ((-1.0, -1.0, -1.0), (1.0, 3.0, 1.0))])    # 2^k, off-centre
+def test_tc_render_box(lo, hi):
+    """Other bounding boxes: extents that are not powers of two take the kernel's general
+    texel-coordinate path (IEEE division), power-of-two extents its multiply fast path."""
+    w = _wl(C=32, L=4, H=24, W=20, N=64)
+    tp, intr, c2w, mlp = dev_workload(w)
+    rgb, alpha = api.dmv3d_render_views(tp, intr, c2w, 24, 20, mlp, samples_per_ray=64, term_eps=1e-4,
+                                        engine="tcgen05", aabb_min=lo, aabb_max=hi)
+    orgb, oalpha = oracle.render_views(w.triplane, w.cameras, w.mlp, 64, oracle.AGG_MEAN,
+                                       aabb_min=lo, aabb_max=hi)
+    er, ea = _report(rgb.cpu().numpy(), alpha.cpu().numpy(), orgb, oalpha)
+    assert er < RGB_TOL and ea < ALPHA_TOL
+    assert 0.0 < float(alpha.mean()) < 1.0
+
+
 def test_tc_cfg3_sampled():
     """The benchmark configuration itself (8 views 256^2, C=80, N=128), sampled."""
     w = wl.make_workload("cfg3")
