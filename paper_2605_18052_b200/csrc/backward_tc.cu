@@ -53,18 +53,18 @@ namespace dmv3d {
 namespace {
 
 constexpr int kHD = 64;        // hidden width
-constexpr int kKW = 64;        // max staged texels per blend window
+constexpr int kKW = 96;        // max staged texels per blend window (128^2 crops: most chunks fit)
 constexpr int kPatch = 4;      // 4x4 rays per patch
 constexpr int kChunk = 8;      // samples per ray per tile
 constexpr uint32_t kHK = kHD + 16;          // h tile columns: 64 activations + [1, 0 x 15]
 constexpr uint32_t kHSbo = (kHK / 8) * 128;   // 1280: stride of 8-row groups in an h tile
 constexpr uint32_t kHBytes = 128 * kHK * 2;   // 20 KiB
-// sparse A tile: 8-row groups 1024 + 32 B apart, so rows m, m+8, m+16, m+24 of a warp
-// fall into different banks in the 2-byte weight scatter (as in render_tc); the tile is
-// rounded up to 17 KiB so every group's B tile stays 1 KiB aligned
-constexpr uint32_t kASbo = (kKW / 8) * 128 + 32;  // 1056
-constexpr uint32_t kABytes = 17 * 1024;           // >= 16 * kASbo
-constexpr uint32_t kBBytes = kKW * kHD * 2;   // 8 KiB (SWIZZLE_128B texel rows); later d_o
+// sparse A tile: 8-row groups (kKW / 8) * 128 + 32 B apart, so rows m, m+8, m+16, m+24 of
+// a warp fall into different banks in the 2-byte weight scatter (as in render_tc); the
+// tile is rounded up to whole KiB so every group's B tile stays 1 KiB aligned
+constexpr uint32_t kASbo = (kKW / 8) * 128 + 32;                // 1568
+constexpr uint32_t kABytes = ((16 * kASbo + 1023) / 1024) * 1024;  // 25 KiB
+constexpr uint32_t kBBytes = kKW * kHD * 2;   // 12 KiB (SWIZZLE_128B texel rows); later d_o
 constexpr uint32_t kDoSbo = 256;              // d_o tile [128][16]: 2 column blocks
 constexpr uint32_t kWK = kHD + 16;
 constexpr uint32_t kWSbo = (kWK / 8) * 128;   // 1280
