@@ -397,8 +397,13 @@ __global__ void __launch_bounds__(128 * NG, 1)
     auto scatter_a = [&](int w0) {
       const int kp = min(kKW, ktot - w0);
       const bool one_window = ktot <= kKW;
-#pragma unroll
-      for (int kc = 0; kc < kKW / 8; ++kc) ptx::sts128(sArow + (uint32_t)(kc << 7), 0u, 0u, 0u, 0u);
+      // zero the window's kpad columns (a plain loop of two 16-B stores, as in render_tc)
+      const int kpz = (kp + 15) & ~15;
+#pragma unroll 1
+      for (int kc = 0; kc < kpz / 16; ++kc) {
+        ptx::sts128(sArow + (uint32_t)(kc << 8), 0u, 0u, 0u, 0u);
+        ptx::sts128(sArow + (uint32_t)((kc << 8) + 128), 0u, 0u, 0u, 0u);
+      }
       if (!sv) return;
       const int base1 = ext0 * ext1, base2 = base1 + ext0 * ext2;
       const int ca = ix[0] - lo0, cb = ix[1] - lo1, cc = ix[2] - lo2;
